@@ -1,0 +1,132 @@
+/*
+ * sketchrecon_b200 -- C ABI of the B200 (sm_100a) sketched SENSE normal-operator path.
+ *
+ * Drop-in boundary for the reference package `sketchrecon`
+ * (/root/reference/pkg/src/sketchrecon).  The reference is pure Python/NumPy and
+ * has no FFI of its own; its plugin seams are the duck-typed Fourier kernel
+ * (`apply` / `apply_adjoint`, linops.py:332-364, forward_model.py:134,147-148)
+ * and the SenseOperator / solver API (forward_model.py:119-224, solvers.py,
+ * coil_sketch.py).  Each entry point below names the reference computation it
+ * replaces.  The Python host package `paper_2305_06482_b200` binds these with
+ * ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - complex64 = interleaved (re, im) float32 (`sr_c64`); all array pointers
+ *     are DEVICE pointers owned by the caller; sizes are element counts.
+ *   - images are C-order (batch, ny, nx); coil stacks (batch, C, ny, nx);
+ *     a *_bstride of 0 shares one array across the batch.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *     asynchronous and stream-ordered; none synchronises with the host.
+ *   - return 0 on success, 1 invalid argument / shape (the reference raises
+ *     ValueError), 2 unsupported transform length, 3 CUDA launch error.
+ *   - FFT lengths: sr_fft_size_supported(n) (2^a 3^b 5^c with a register split,
+ *     e.g. 8..1024 powers of two, 10..640 x5, 200, 400, 800, 24..768 x3).
+ *   - Spectrum layout: the 2-D spectrum kept in `ws` is in "perm order" along
+ *     both axes: frequency k of an n = P*Q axis sits at P*(k % Q) + k / Q.
+ *     `maskT`, `spos` are built by the host in that layout.
+ */
+#ifndef SKETCHRECON_B200_H
+#define SKETCHRECON_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { float x, y; } sr_c64;
+
+/* 1 if an axis of length n has an instantiated FFT. */
+int sr_fft_size_supported(int n);
+/* (P, Q) register split of an axis of length n = P*Q (perm order P*(k % Q) + k / Q). */
+int sr_fft_split(int n, int* P, int* Q);
+
+/* K1 -- fused Cartesian (sketched) SENSE normal operator, batched over slices.
+ *   out_b = e( sum_j conj(c_bj) * F^H M'_b F (c_bj * (x_b - anchor_b)) )
+ * replaces `a_s.adjoint(a_s.forward(v))` (forward_model.py:168-180 over
+ * linops.py:344-364), the call made at coil_sketch.py:126,133,197 and
+ * solvers.py:175,248,460.
+ *   maps: (batch, ncoils, ny, nx), map_bstride elements between slices (0 = shared)
+ *   maskT: uint8 (ny*nx per mask) sampled-bin indicator, transposed [pos_x][pos_y]
+ *          in perm order; mask_bstride bytes between slices (0 = shared)
+ *   ws: workspace of batch*ncoils*ny*nx complex64
+ *   anchor: NULL or (batch, ny, nx): operator input is x - anchor
+ *   coef: NULL -> out = acc; else device float4 per slice {s_acc, s_u, s_d, -}:
+ *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v) */
+int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
+                   long long map_bstride, const uint8_t* maskT, long long mask_bstride,
+                   sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
+                   const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+
+/* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
+ * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)
+ * over `_CartesianMaskKernel.apply` (linops.py:344-352).
+ *   spos/ph: per-sample perm-order spectrum offset and centering phase; slice b owns
+ *            samples [soff[b], soff[b+1]); y is (batch, ncoils, ystride)
+ *   ymeas: NULL, or measured data -> y = A x - ymeas and, if partial != NULL,
+ *          partial[(b*ncoils + j)*partial_blocks + k] = sum |y|^2 pieces
+ *          (the residual of composite_objective, solvers.py:188-195). */
+int sr_cart_forward(const sr_c64* x, const sr_c64* maps, long long map_bstride,
+                    const int* spos, const sr_c64* ph, const long long* soff,
+                    sr_c64* y, long long ystride, const sr_c64* ymeas, double* partial,
+                    int partial_blocks, sr_c64* ws, int batch, int ncoils, int ny, int nx,
+                    void* stream);
+
+/* K2 -- SENSE adjoint A^H y: scatter (last duplicate wins, as numpy fancy
+ * assignment at linops.py:357), centered unitary IFFT, conjugate coil sum
+ * (forward_model.py:174-180).  wlist/woff: per-slice list of sample indices to
+ * write (duplicates removed by the host).  coef/u/d: epilogue as sr_cart_normal. */
+int sr_cart_adjoint(const sr_c64* y, long long ystride, const sr_c64* maps,
+                    long long map_bstride, const int* spos, const sr_c64* ph,
+                    const long long* soff, const int* wlist, const long long* woff,
+                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
+                    const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+
+/* K5 -- coil contraction out[b,i,:] = sum_k S[b,i,k] in[b,k,:]:
+ * `sketch_maps` (sketching.py:97-103, S real Chat x C) and the map/data rotation
+ * of `coil_compress_svd` (forward_model.py:268-269, S = comp complex keep x C).
+ * s_bstride = 0 shares S across the batch. in and out must not alias. */
+int sr_coil_contract(const sr_c64* in, sr_c64* out, const sr_c64* S, long long s_bstride,
+                     int batch, int cout, int cin, long long D, long long in_bstride,
+                     long long out_bstride, void* stream);
+
+/* K6 -- one level of the 2-D periodic DB4 analysis (linops.py:619-635, 677-687)
+ * on the top-left h x w corner (row stride ld, slice stride bs); optional fused
+ * soft threshold (solvers.py:129-135) with per-slice thresh[] (device) or host
+ * hthresh >= 0; `last` thresholds the low-pass corner too; l1part collects
+ * sum |coef| (Regularizer.value, solvers.py:61-69). src and dst must differ. */
+int sr_wavelet_ana2(const sr_c64* src, sr_c64* dst, int h, int w, int ld, long long bs,
+                    int batch, const float* thresh, float hthresh, int last, double* l1part,
+                    void* stream);
+int sr_wavelet_ana2_nblocks(int h, int w);
+/* K6 -- one level of 2-D synthesis (linops.py:638-651, 689-702); at the final
+ * level an optional FISTA momentum epilogue z = x + beta (x - xold)
+ * (solvers.py:292-293). coef and out must differ. */
+int sr_wavelet_syn2(const sr_c64* coef, sr_c64* out, int h, int w, int ld, long long bs,
+                    int batch, sr_c64* zout, const sr_c64* xold, float beta, void* stream);
+int sr_wavelet_levels_max(void);
+
+/* K7 -- deterministic per-slice reductions (fixed-order, no atomics).
+ * mode 0: sum |a|^2   1: sum conj(a) b   2: sum |a|   3: sum |a - b|^2
+ * partial: batch * sr_reduce_nparts() double2; result: batch double2.
+ * (np.linalg.norm / np.vdot in solvers.py:192,211,219,225 and linops.py:777-780) */
+int sr_reduce(int mode, const sr_c64* a, const sr_c64* b, long long n, long long bstride,
+              int batch, double* partial, double* result, void* stream);
+int sr_reduce_nparts(void);
+
+/* K7 -- out = cx*X + cy*Y + cz*Z with per-slice device coefficients (float4) or
+ * host coefficients when coef == NULL (axpy / momentum of solvers.py:223-227,293). */
+int sr_lincomb(sr_c64* out, const sr_c64* X, const sr_c64* Y, const sr_c64* Z,
+               const float* coef, float cx, float cy, float cz, long long n,
+               long long bstride, int batch, void* stream);
+
+/* K7 -- per-slice scalar bookkeeping on the device:
+ * op 0 power iteration step (linops.py:776-781), op 1 CG alpha, op 2 CG beta
+ * (solvers.py:218-228). */
+int sr_scalar_op(int op, const double* in0, const double* in1, double* state, float* coefA,
+                 float* coefB, int* flags, int batch, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKETCHRECON_B200_H */

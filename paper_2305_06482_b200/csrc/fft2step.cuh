@@ -1,0 +1,84 @@
+// Two-level (four-step) in-CTA FFT building blocks.
+//
+// A length N = P*Q transform is split as natural index m = p + P*q
+// (p < P, q < Q).  Frequencies k = k2 + Q*k1 (k2 < Q, k1 < P).
+//
+//   forward step 1 (per p, in registers):  Y[p][k2] = DFT_Q over q of x[p + P q],
+//                                           then *= W_N^{p k2}; stored at pos P*k2 + p
+//   forward step 2 (per k2, in registers): X[k2 + Q k1] = DFT_P over p of Y[p][k2];
+//                                           stored at pos P*k2 + k1      ("perm order")
+//   inverse step 2' (per k2): DFT^-1_P over k1 of the perm-order group, *= conj W_N^{m1 k2}
+//   inverse step 1' (per m1): DFT^-1_Q over k2 -> x[m1 + P m2] in natural order.
+//
+// The forward output is left in perm order and the inverse consumes perm
+// order, so forward -> (pointwise op) -> inverse never reorders data; the
+// pointwise op (the undersampling mask) is stored in perm order by the host.
+//
+// Shared-memory layout: one vector of N float2 occupies Q groups of P
+// elements, each group padded by one element (stride P+1) so that both the
+// strided step-1 access and the contiguous step-2 access are bank-conflict
+// free for P in {8, 16, 32}.
+#pragma once
+#include "common.cuh"
+#include "dft_gen.cuh"
+
+template <int P_, int Q_>
+struct FftShape {
+  static constexpr int P = P_;
+  static constexpr int Q = Q_;
+  static constexpr int N = P_ * Q_;
+  static constexpr int GS = (P_ == 1) ? 1 : P_ + 1;  // padded group stride
+  static constexpr int VS = Q_ * GS;                  // padded vector length
+  __device__ __forceinline__ static int pad(int pos) { return (P_ == 1) ? pos : pos + pos / P_; }
+  // perm position of frequency k (forward output layout)
+  __host__ __device__ __forceinline__ static int perm_pos(int k) { return P_ * (k % Q_) + k / Q_; }
+};
+
+// tw[m] = exp(-2 pi i m / N), m in [0, N): double-precision sincospi, rounded once.
+template <int N>
+__device__ __forceinline__ void init_twiddles(float2* tw, int tid, int nthreads) {
+  for (int m = tid; m < N; m += nthreads) {
+    double s, c;
+    sincospi(-2.0 * (double)m / (double)N, &s, &c);
+    tw[m] = make_float2((float)c, (float)s);
+  }
+}
+
+// forward step 1: r[q] = x[p + P q]  ->  r[k2] = W_N^{p k2} * DFT_Q(r)[k2]
+template <int P, int Q>
+__device__ __forceinline__ void fft_s1_fwd(float2* r, int p, const float2* tw) {
+  RegDFT<Q, false>::run(r);
+  if (P > 1) {
+#pragma unroll
+    for (int k2 = 1; k2 < Q; ++k2) r[k2] = cmul(r[k2], tw[p * k2]);
+  }
+}
+
+// forward step 2: group of P values (index p) -> DFT_P (index k1)
+template <int P>
+__device__ __forceinline__ void fft_s2_fwd(float2* g) { RegDFT<P, false>::run(g); }
+
+// inverse step 2': group (index k1) -> IDFT_P (index m1), then *= conj(W_N^{m1 k2})
+template <int P, int Q>
+__device__ __forceinline__ void fft_s2_inv(float2* g, int k2, const float2* tw) {
+  RegDFT<P, true>::run(g);
+  if (Q > 1) {
+#pragma unroll
+    for (int m1 = 1; m1 < P; ++m1) g[m1] = cmulc(tw[m1 * k2], g[m1]);
+  }
+}
+
+// inverse step 1': r[k2] -> IDFT_Q -> r[m2] = x[m1 + P m2]
+template <int Q>
+__device__ __forceinline__ void fft_s1_inv(float2* r) { RegDFT<Q, true>::run(r); }
+
+// ---------------------------------------------------------------------------
+// Supported lengths and their (P, Q) split.  X(N, P, Q)
+#define SR_FFT_SIZES(X)                                                          \
+  X(1, 1, 1) X(2, 1, 2) X(3, 1, 3) X(4, 1, 4) X(5, 1, 5) X(6, 1, 6) X(8, 1, 8)             \
+  X(10, 1, 10) X(12, 1, 12) X(16, 1, 16) X(20, 1, 20) X(24, 1, 24) X(25, 1, 25) \
+  X(32, 16, 2) X(40, 8, 5) X(48, 16, 3) X(50, 2, 25) X(64, 16, 4)               \
+  X(80, 16, 5) X(96, 16, 6) X(100, 4, 25) X(128, 16, 8) X(160, 16, 10)          \
+  X(192, 16, 12) X(200, 8, 25) X(256, 16, 16) X(320, 16, 20) X(384, 16, 24)     \
+  X(400, 16, 25) X(512, 16, 32) X(640, 32, 20) X(768, 32, 24) X(800, 32, 25)    \
+  X(1024, 32, 32)

@@ -1,0 +1,115 @@
+"""Pin the CPU oracle against golden vectors produced by the real reference.
+
+tests/golden/*.npz come from tests/golden/make_golden.py, which imports
+/root/reference/pkg/src/sketchrecon and runs it on seeded inputs.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel
+from oracle import sketch_oracle as O
+
+TOL = 1e-10
+
+
+def test_rng_and_sketch_draws():
+    g = golden("rng")
+    assert [O.child_seed(0, t) for t in range(1, 6)] == list(g["child_seeds"])
+    # SURVEY 8c survey-time values
+    assert list(g["child_seeds"][:3]) == [3964924996, 3141116543, 2613022947]
+    m = O.gen_sketch_matrix(12, 6, 6, 32, int(g["child_seeds"][0]))
+    np.testing.assert_array_equal(m, g["sketch_12_6_6_c32"])
+    np.testing.assert_array_equal(m[6, 6:16], [-1, 1, 1, -1, -1, -1, 1, -1, -1, 1])
+    np.testing.assert_array_equal(O.gen_sketch_matrix(4, 2, 2, 9, 7, "gaussian"), g["sketch_gauss"])
+    gs = O.seed_stream(0, 0)
+    v0 = gs.standard_normal(50) + 1j * gs.standard_normal(50)
+    np.testing.assert_array_equal(v0, g["power_v0"])
+
+
+def test_centered_fft_kats():
+    g = golden("fft")
+    d8 = np.zeros((8, 8), complex)
+    d8[4, 4] = 1
+    assert rel(O.centered_dft(d8, 2).ravel(), g["delta8"]) < TOL
+    np.testing.assert_allclose(g["delta8"], 1 / 8)
+    assert rel(O.centered_dft(np.ones((8, 8), complex), 2).ravel(), g["ones8"]) < TOL
+    assert rel(O.centered_dft(g["x"], 2).ravel(), g["fx"]) < TOL
+    assert rel(O.centered_dft(g["x"], 2, inverse=True).ravel(), g["ifx"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["sense_cart", "sense_cart_b", "sense_cart_1d"])
+def test_cartesian_sense(name):
+    g = golden(name)
+    dims = tuple(g["dims"])
+    k = O.CartesianKernel(dims, g["points"])
+    a = O.Sense(g["maps"], k)
+    assert rel(a.forward(g["x"]), g["Ax"]) < TOL
+    assert rel(a.adjoint(g["y"]), g["AHy"]) < TOL
+    assert rel(a.normal(g["x"]), g["AHAx"]) < TOL
+    smaps = g["S"] @ g["maps"]
+    assert rel(smaps, g["smaps"]) < TOL
+    a_s = O.Sense(smaps, k)
+    assert rel(a_s.normal(g["x"]), g["AsHAsx"]) < TOL
+    lam = O.power_max_eig(a_s.normal, int(np.prod(dims)))
+    assert abs(lam - float(g["lam_max"])) < 1e-10 * abs(float(g["lam_max"]))
+
+
+@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24"])
+def test_wavelet(name):
+    g = golden(name)
+    dims = tuple(g["dims"])
+    assert O.wavelet_levels(dims) == int(g["levels"])
+    assert rel(O.wavelet_forward(g["x"], dims), g["fwd"]) < TOL
+    assert rel(O.wavelet_adjoint(g["x"], dims), g["adj"]) < TOL
+    assert rel(O.wavelet_prox(g["x"], dims, 0.7, 0.3), g["prox"]) < TOL
+    assert abs(O.wavelet_l1(g["x"], dims, 0.3) - float(g["value"])) < 1e-10 * float(g["value"])
+    # unitary round trip (SPEC 68-70)
+    assert rel(O.wavelet_adjoint(O.wavelet_forward(g["x"], dims), dims), g["x"]) < 1e-12
+
+
+@pytest.mark.parametrize("name", ["nufft_2x_w4", "nufft_125_w4", "nufft_125_w6", "nufft3d"])
+def test_gridded_nufft(name):
+    g = golden(name)
+    dims = tuple(g["dims"])
+    k = O.GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    assert rel(k.apply(g["batch"]), g["fwd"]) < TOL
+    assert rel(k.apply_adjoint(g["y"]), g["adj"]) < TOL
+    if "AHAx" in g:
+        w = O.radial_density_weights(g["points"])
+        assert rel(w, g["weights"]) < 1e-14
+        a = O.Sense(g["maps"], k, w)
+        assert rel(a.normal(g["x"]), g["AHAx"]) < TOL
+
+
+def test_coil_compression():
+    g = golden("compress")
+    d, m, comp, en = O.coil_compress_svd(g["data"], g["maps"], 4)
+    assert rel(comp, g["comp"]) < TOL
+    assert rel(d, g["cdata"]) < TOL and rel(m, g["cmaps"]) < TOL
+    assert abs(en - float(g["energy"])) < 1e-12
+
+
+def _kernel_for(g):
+    dims = tuple(g["dims"])
+    if float(g["oversamp"]) > 0:
+        return lambda: O.GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    return lambda: O.CartesianKernel(dims, g["points"])
+
+
+@pytest.mark.parametrize("name,solver,reg", [("recon_cart", "fista", "l1-wavelet"),
+                                             ("recon_cart_pm1", "fista", "l1-wavelet"),
+                                             ("recon_cart_cg", "cg", "l2"),
+                                             ("recon_radial", "fista", "l1-wavelet")])
+def test_recon_end_to_end(name, solver, reg):
+    g = golden(name)
+    dims = tuple(g["dims"])
+    w = g["weights"] if g["weights"].size else None
+    res = O.coil_sketching_recon(g["data"], g["maps"], dims, _kernel_for(g), c_hat0=int(g["chat0"]),
+                                 v=int(g["v"]), s=int(g["s"]), lam=float(g["lam"]), outer=int(g["outer"]),
+                                 inner=int(g["inner"]), seed=0, weights=w,
+                                 rademacher_scale=float(g["scale"]), solver=solver, reg=reg)
+    assert rel(res.x_final, g["x_final"]) < 1e-9
+    np.testing.assert_allclose(res.objectives, g["objectives"], rtol=1e-9)
+    assert res.counts["coil_transform"] == int(g["counts"]) == int(g["expected"])
+    assert res.diverged == bool(g["diverged"])
