@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""Benchmark: sketched SENSE normal-operator applies/s (BASELINE.json config 1).
+
+Workload (config 1): 64 independent 320x320 slices, 32 Gaussian coils, VD
+Poisson-disc masks R=6 with a 24x24 centre (one per slice), PCA compression
+from simulated noisy data, sketch 6 PCA + 6 Rademacher(+-1/sqrt(12)) coils.
+One step = one sketched normal-op apply A_s^H A_s x over all 64 slices
+(the K1 kernel: 3 launches).  Inputs: 629 MB of sketched maps alone, larger
+than the 126 MB L2, so no explicit flush between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched with torchrun: each rank owns its own 64-slice batch
+(independent slices; no collective on the data path) -> weak scaling.
+`--impl reference` times the CPU oracle port (oracle/sketch_oracle.py, a
+restatement of the pure-NumPy reference) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+NSLICE, NY, NX, C_FULL, V, S = 64, 320, 320, 32, 6, 6
+ACCEL, CALIB = 6.0, 24
+CHAT = V + S
+SCALE = 1.0 / math.sqrt(12.0)
+METRIC = "sketched normal-op applies/s (64 x 320^2 slices, C=32 -> C_hat=12)"
+UNIT = "applies/s"
+
+
+def algorithmic_bytes(nslice=NSLICE, D=NY * NX, chat=CHAT):
+    """slices * 8 * D * (C_hat + 2) + bit-packed mask per distinct mask."""
+    return nslice * 8 * D * (chat + 2) + nslice * D / 8
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                self.samples.append((sm, rs, util))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if self.nv is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        nv = self.nv
+        names = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        busy = [s for s in self.samples if s[2] > 0] or self.samples
+        reasons = set()
+        for _, rs, _ in busy:
+            for n, bit in names.items():
+                if n != "gpu_idle" and rs & bit:
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median([s[0] for s in busy])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(seed: int, dev):
+    """Device-resident config-1 inputs; returns dict of tensors and host tables."""
+    import torch
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    from paper_2305_06482_b200.sketching import coil_contract, gen_sketch_matrix, SketchConfig
+    from paper_2305_06482_b200.rng import child_seed
+
+    rng = np.random.default_rng(seed)
+    dims = (NY, NX)
+    D = NY * NX
+    masks = synth.vd_poisson_masks(dims, ACCEL, CALIB, [seed * 1000 + b for b in range(NSLICE)])
+    pts = [synth.mask_points(m) for m in masks]
+    kern = CartesianKernel(dims, [cartesian_plan(dims, p) for p in pts])
+    maps = torch.empty(NSLICE, C_FULL, D, dtype=torch.complex64, device=dev)
+    for b in range(NSLICE):
+        maps[b] = synth.gaussian_coil_maps(dims, C_FULL, rng, xp=torch, device=dev)
+    img = np.stack([synth.random_ellipses(dims, 10, rng).ravel() for _ in range(NSLICE)])
+    x_true = torch.from_numpy(img.astype(np.complex64)).to(dev)
+    # acquisition: y = A x + noise, sigma = 0.01 max|k| (per slice)
+    y = kern.forward(maps, x_true)
+    sig = 0.01 * torch.abs(y).reshape(NSLICE, -1).amax(dim=1)
+    noise = torch.randn(y.shape, dtype=torch.complex64, device=dev, generator=torch.Generator(dev).manual_seed(seed))
+    y = y + noise * sig.view(-1, 1, 1).to(torch.complex64)
+    # PCA coil compression (keep = C) from the data SVD, batched on the device
+    for b in range(NSLICE):
+        n = kern.n_points_per_slice[b]
+        y[b, :, n:] = 0
+    u, _, _ = torch.linalg.svd(y, full_matrices=False)
+    comp = u.conj().transpose(1, 2).contiguous()  # (B, C, C)
+    maps0 = coil_contract(maps, comp)
+    del maps
+    sk = gen_sketch_matrix(SketchConfig(CHAT, V, S, "rademacher", child_seed(seed, 1), rademacher_scale=SCALE), C_FULL)
+    smaps = coil_contract(maps0, sk.mat)
+    x = x_true.clone()
+    torch.cuda.synchronize()
+    return dict(kern=kern, maps0=maps0, smaps=smaps, x=x, pts=pts)
+
+
+def time_applies(fn, steps, warmup, sync_fn):
+    import torch
+    for _ in range(warmup):
+        fn()
+    sync_fn()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        fn()
+    stop.record()
+    sync_fn()
+    return start.elapsed_time(stop) / 1e3
+
+
+# ------------------------------------------------------------------ CPU baseline
+def _oracle_slice_task(args):
+    b, seed = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import sketch_oracle as O
+    from paper_2305_06482_b200 import synth
+    rng = np.random.default_rng(seed * 7919 + b)
+    dims = (NY, NX)
+    m = synth.vd_poisson_mask(dims, ACCEL, CALIB, seed * 1000 + b)
+    kern = O.CartesianKernel(dims, synth.mask_points(m))
+    maps = synth.gaussian_coil_maps(dims, CHAT, rng)
+    x = synth.random_ellipses(dims, 10, rng).ravel()
+    return kern, maps, x
+
+
+_POOL_STATE = {}
+
+
+def _pool_init(seed, slices):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    _POOL_STATE["ops"] = {b: _oracle_slice_task((b, seed)) for b in slices}
+
+
+def _pool_apply(b):
+    from oracle import sketch_oracle as O
+    kern, maps, x = _POOL_STATE["ops"][b]
+    return float(np.abs(O.Sense(maps, kern).normal(x)[0]))
+
+
+def cpu_baseline_single(seed: int, budget_s: float = 10.0):
+    """Oracle (complex128 numpy) sketched normal op, one process; scaled to the 64-slice unit."""
+    from oracle import sketch_oracle as O
+    n, t = 0, 0.0
+    while t < budget_s and n < NSLICE:
+        kern, maps, x = _oracle_slice_task((n, seed))
+        t0 = time.perf_counter()
+        O.Sense(maps, kern).normal(x)
+        t += time.perf_counter() - t0
+        n += 1
+    per_slice = t / n
+    return {"value": 1.0 / (per_slice * NSLICE), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n} of the 64 slices (320^2, C_hat=12) through the oracle's sketched normal op "
+                      f"(numpy complex128, single process), extrapolated to one 64-slice apply"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on all host cores, same workload and metric."""
+    import concurrent.futures as cf
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    workers = max(1, min(cores, NSLICE))
+    slices = list(range(NSLICE))
+    chunks = [slices[i::workers] for i in range(workers)]
+    ctx = __import__("multiprocessing").get_context("fork")
+    pools = []
+    # one single-worker pool per chunk so each worker owns its slices' inputs
+    for ch in chunks:
+        pools.append((cf.ProcessPoolExecutor(1, mp_context=ctx, initializer=_pool_init, initargs=(args.seed, ch)), ch))
+
+    def step():
+        futs = [p.submit(_run_chunk, ch) for p, ch in pools]
+        for f in futs:
+            f.result()
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    for p, _ in pools:
+        p.shutdown()
+    value = args.steps / el
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "config1: 64 x 320x320 slices, C_hat=12 sketched normal op",
+                       "slices": NSLICE, "dims": [NY, NX], "c_hat": CHAT},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                             "sample": "full 64-slice apply per step, oracle numpy complex128, one process per core"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _run_chunk(ch):
+    return [_pool_apply(b) for b in ch]
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2305_06482_b200 import _lib
+    _lib.lib()
+    w = build_workload(args.seed + rank, dev)
+    kern, smaps, maps0, x = w["kern"], w["smaps"], w["maps0"], w["x"]
+    out = torch.empty_like(x)
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def apply_sketched():
+        kern.normal(smaps, x, out)
+
+    def apply_full():
+        kern.normal(maps0, x, out)
+
+    with ClockSampler(local) as clk:
+        t_s = time_applies(apply_sketched, args.steps, args.warmup, barrier_sync)
+    t_full = time_applies(apply_full, max(3, args.steps // 5), 2, barrier_sync)
+
+    # e2e through the public operator call with pinned host buffers
+    x_host = x.cpu().pin_memory()
+    out_host = torch.empty_like(x_host).pin_memory()
+    x_dev = torch.empty_like(x)
+
+    def e2e_step():
+        x_dev.copy_(x_host, non_blocking=True)
+        kern.normal(smaps, x_dev, out)
+        out_host.copy_(out, non_blocking=True)
+
+    t_e2e = time_applies(e2e_step, max(5, args.steps // 2), 2, barrier_sync)
+    n_e2e = max(5, args.steps // 2)
+
+    def maxr(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    t_s, t_full, t_e2e = maxr(t_s), maxr(t_full), maxr(t_e2e)
+    value = world * args.steps / t_s
+    ms = t_s / args.steps * 1e3
+    bytes_apply = algorithmic_bytes()
+    peak, peak_kind = measured_peak()
+    achieved = bytes_apply / (t_s / args.steps) / 1e9
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline else cpu_baseline_single(args.seed)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": "config1: 64 x 320x320 slices, C=32 -> C_hat=12 (6 PCA + 6 Rademacher "
+                                   "+-1/sqrt(12)), VD Poisson-disc R=6 per slice, one sketched normal-op apply",
+                       "slices": NSLICE, "dims": [NY, NX], "coils": C_FULL, "c_hat": CHAT,
+                       "l2": "inputs (629 MB sketched maps) exceed the 126 MB L2; no flush",
+                       "parallelism": f"slices, {world} independent rank(s)"},
+            "e2e": {"value": world * n_e2e / t_e2e, "unit": UNIT,
+                    "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8),
+                    "path": "pinned host x -> CartesianKernel.normal -> pinned host out"},
+            "unsketched_32coil": {"value": world * max(3, args.steps // 5) / t_full, "unit": UNIT,
+                                  "speedup_sketched": (world * args.steps / t_s) / (world * max(3, args.steps // 5) / t_full)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "K1 fused sketched normal op (rowfwd + colpass + rowinv launches)",
+                         "algorithmic_bytes_per_apply": bytes_apply},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

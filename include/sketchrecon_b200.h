@@ -126,6 +126,13 @@ int sr_lincomb(sr_c64* out, const sr_c64* X, const sr_c64* Y, const sr_c64* Z,
 int sr_scalar_op(int op, const double* in0, const double* in1, double* state, float* coefA,
                  float* coefB, int* flags, int batch, void* stream);
 
+/* Host (CPU) synthetic-input helper: variable-density Poisson-disc mask of
+ * ny x nx bins (1 = sampled, row-major) with a fully sampled calib x calib
+ * centre and about ny*nx/accel samples (BASELINE configs 0-2; the reference
+ * only has 1-D line masks, simulate.py:209-259).  Returns the sample count. */
+long long sr_host_vd_poisson(int ny, int nx, double accel, int calib, unsigned long long seed,
+                             uint8_t* mask);
+
 #ifdef __cplusplus
 }
 #endif

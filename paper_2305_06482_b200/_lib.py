@@ -34,7 +34,9 @@ SIGNATURES = {
     "sr_reduce_nparts": [],
     "sr_lincomb": [_vp, _vp, _vp, _vp, _vp, _f, _f, _f, _ll, _ll, _i, _vp],
     "sr_scalar_op": [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp],
+    "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
 }
+RESTYPES = {"sr_host_vd_poisson": C.c_longlong}
 
 _ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError}
 _MESSAGES = {1: "invalid argument or shape", 2: "unsupported transform length",
@@ -60,7 +62,7 @@ def lib():
         for name, args in SIGNATURES.items():
             fn = getattr(handle, name)
             fn.argtypes = args
-            fn.restype = C.c_int
+            fn.restype = RESTYPES.get(name, C.c_int)
         _lib = handle
     return _lib
 

@@ -1,0 +1,155 @@
+"""Cartesian Fourier kernel on the device (K1 normal op, K2 forward/adjoint).
+
+Drop-in for the reference plugin ``_CartesianMaskKernel``
+(/root/reference/pkg/src/sketchrecon/linops.py:332-364): it exposes the same
+``n_points`` / ``apply`` / ``apply_adjoint`` protocol (host numpy, used when it
+is plugged into a reference ``SenseOperator``) and, for the performance path,
+batched device entry points that fuse the map multiply, both FFT passes, the
+mask and the conjugate coil sum (``normal``), plus ``forward``/``adjoint``
+with compact samples in trajectory order.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .plan import CartesianPlan, cartesian_plan, grid2d
+
+
+def _no_weights(w):
+    if w is not None:
+        raise ValueError("density weights are not used with Cartesian masks")
+
+
+class CartesianKernel:
+    """Device tables for B slices sharing one grid (one mask per slice or shared).
+
+    ``plans`` holds one CartesianPlan per slice (len B) or a single shared plan.
+    """
+
+    def __init__(self, dims, plans: list[CartesianPlan], batch: int | None = None):
+        self.dims = tuple(int(n) for n in dims)
+        self.ny, self.nx = grid2d(self.dims)
+        for n in (self.ny, self.nx):
+            if n > 1 and not _lib.lib().sr_fft_size_supported(n):
+                raise ValueError(f"grid axis {n} has no sm_100a FFT instantiation")
+        self.D = self.ny * self.nx
+        self.batch = int(batch if batch is not None else len(plans))
+        if len(plans) not in (1, self.batch):
+            raise ValueError("need one plan per slice or one shared plan")
+        self.shared_mask = len(plans) == 1
+        per_slice = plans if len(plans) == self.batch else plans * self.batch
+        self.n_points_per_slice = [p.n_points for p in per_slice]
+        self.n_points = per_slice[0].n_points
+        self.nmax = max(self.n_points_per_slice)
+        dev = dv.require_cuda()
+        self.device = dev
+        self.maskT = dv.host_to_dev(np.stack([p.maskT for p in plans]), torch.uint8, dev)
+        self.mask_bstride = 0 if self.shared_mask else self.D
+        self.spos = dv.host_to_dev(np.concatenate([p.spos for p in per_slice]), torch.int32, dev)
+        self.ph = dv.c64(np.concatenate([p.ph for p in per_slice]), dev)
+        soff = np.zeros(self.batch + 1, dtype=np.int64)
+        soff[1:] = np.cumsum(self.n_points_per_slice)
+        self.soff = dv.host_to_dev(soff, torch.int64, dev)
+        self.wlist = dv.host_to_dev(np.concatenate([p.wlist for p in per_slice]), torch.int32, dev)
+        woff = np.zeros(self.batch + 1, dtype=np.int64)
+        woff[1:] = np.cumsum([len(p.wlist) for p in per_slice])
+        self.woff = dv.host_to_dev(woff, torch.int64, dev)
+        self._ws = None
+        self._plans = plans
+        self._replicas: dict[int, "CartesianKernel"] = {}
+
+    @classmethod
+    def from_points(cls, dims, points) -> "CartesianKernel":
+        return cls(dims, [cartesian_plan(tuple(dims), points)])
+
+    # ------------------------------------------------------------------ device
+    def workspace(self, ncoils: int, batch: int | None = None) -> torch.Tensor:
+        need = (batch or self.batch) * ncoils * self.D
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.complex64, device=self.device)
+        return self._ws
+
+    def _maps_stride(self, maps: torch.Tensor) -> tuple[int, int]:
+        if maps.dim() != 3 or maps.shape[2] != self.D or maps.shape[0] not in (1, self.batch):
+            raise ValueError(f"maps must be (1 or {self.batch}, C, {self.D}), got {tuple(maps.shape)}")
+        if maps.dtype != torch.complex64 or not maps.is_contiguous():
+            raise ValueError("maps must be contiguous complex64")
+        ncoils = maps.shape[1]
+        return ncoils, (0 if maps.shape[0] == 1 else ncoils * self.D)
+
+    def _check_img(self, t, name):
+        if t is None:
+            return
+        if t.shape != (self.batch, self.D) or t.dtype != torch.complex64 or not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous complex64 ({self.batch}, {self.D})")
+
+    def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None):
+        """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1)."""
+        _no_weights(w)
+        ncoils, mbs = self._maps_stride(maps)
+        for t, n in ((x, "x"), (out, "out"), (anchor, "anchor"), (u, "u"), (d, "d")):
+            self._check_img(t, n)
+        ws = self.workspace(ncoils)
+        _lib.call("sr_cart_normal", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), mbs,
+                  dv.ptr(self.maskT), self.mask_bstride, dv.ptr(out), dv.ptr(ws), self.batch,
+                  ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), dv.stream())
+        return out
+
+    def forward(self, maps, x, y=None, *, ymeas=None, partial=None, partial_blocks=64, w=None):
+        """y[b, j, :N_b] = A_b x_b  (- ymeas);  partial sums of |y|^2 if requested (K2)."""
+        _no_weights(w)
+        ncoils, mbs = self._maps_stride(maps)
+        self._check_img(x, "x")
+        if y is None:
+            y = torch.zeros(self.batch, ncoils, self.nmax, dtype=torch.complex64, device=self.device)
+        ws = self.workspace(ncoils)
+        _lib.call("sr_cart_forward", dv.ptr(x), dv.ptr(maps), mbs, dv.ptr(self.spos),
+                  dv.ptr(self.ph), dv.ptr(self.soff), dv.ptr(y), y.shape[-1], dv.ptr(ymeas),
+                  dv.ptr(partial), partial_blocks, dv.ptr(ws), self.batch, ncoils, self.ny,
+                  self.nx, dv.stream())
+        return y
+
+    def adjoint(self, maps, y, out, *, coef=None, u=None, d=None, w=None):
+        """out_b = sum_j conj(c_j) A_j^H y_bj  (K2)."""
+        _no_weights(w)
+        ncoils, mbs = self._maps_stride(maps)
+        self._check_img(out, "out")
+        if y.dim() != 3 or y.shape[0] != self.batch or y.shape[1] != ncoils or y.shape[2] < self.nmax:
+            raise ValueError("y must be (B, C, >= nmax)")
+        ws = self.workspace(ncoils)
+        _lib.call("sr_cart_adjoint", dv.ptr(y), y.shape[-1], dv.ptr(maps), mbs, dv.ptr(self.spos),
+                  dv.ptr(self.ph), dv.ptr(self.soff), dv.ptr(self.wlist), dv.ptr(self.woff),
+                  dv.ptr(out), dv.ptr(ws), self.batch, ncoils, self.ny, self.nx, dv.ptr(coef),
+                  dv.ptr(u), dv.ptr(d), dv.stream())
+        return out
+
+    # ------------------------------------------------- reference plugin protocol
+    def _replica(self, c: int) -> "CartesianKernel":
+        if self.batch != 1:
+            raise ValueError("the host plugin protocol is single-slice")
+        if c == 1:
+            return self
+        if c not in self._replicas:
+            self._replicas[c] = CartesianKernel(self.dims, self._plans, batch=c)
+        return self._replicas[c]
+
+    def apply(self, batch: np.ndarray) -> np.ndarray:
+        """(C, D) coil images -> (C, N) samples (linops.py:344-352)."""
+        b = np.asarray(batch)
+        k = self._replica(b.shape[0])
+        ones = torch.ones(1, 1, self.D, dtype=torch.complex64, device=self.device)
+        y = k.forward(ones, dv.c64(b.reshape(b.shape[0], self.D)))
+        return dv.to_numpy128(y[:, 0, : self.n_points])
+
+    def apply_adjoint(self, batch: np.ndarray) -> np.ndarray:
+        """(C, N) samples -> (C, D) coil images (linops.py:354-364)."""
+        b = np.asarray(batch)
+        k = self._replica(b.shape[0])
+        ones = torch.ones(1, 1, self.D, dtype=torch.complex64, device=self.device)
+        out = torch.empty(b.shape[0], self.D, dtype=torch.complex64, device=self.device)
+        k.adjoint(ones, dv.c64(b.reshape(b.shape[0], 1, -1)), out)
+        return dv.to_numpy128(out)

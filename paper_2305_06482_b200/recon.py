@@ -1,0 +1,274 @@
+"""Batched device engine for Algorithm 1 (coil-sketched reconstruction).
+
+Runs B independent slices in lock step (one slice = the reference's
+``coil_sketching_recon``, /root/reference/pkg/src/sketchrecon/coil_sketch.py:220-306):
+
+  per outer t:  d = A^H (A x - y)            (residual from the previous objective, K2)
+                S^t drawn on the host          (coil_sketch.py:276-278, bit-identical)
+                c_hat = S^t c                  (K5)
+                [t == 1] L = lambda_max / s    (30 fused power steps, K1 + K7)
+                inner FISTA / CG               (K1 with fused gradient epilogue, K6 prox
+                                                with fused momentum, K7)
+                objective 0.5||A x - y||^2 + lam ||Psi x||_1 -> residual for t+1
+                divergence check (one host sync per outer)
+
+No host synchronisation inside an inner loop (tol = 0 as in coil_sketch.py:246).
+Counters follow the reference tally per slice: 2*C0 per true gradient,
+2*C_hat per inner iteration; power iteration and objectives are paused.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as dv
+from . import _lib
+from .linops import CostCounter
+from .rng import child_seed, seed_stream
+from .sketching import SketchConfig, coil_contract, gen_sketch_matrix
+from .wavelet import WaveletEngine
+
+DIVERGENCE_FACTOR = 10.0  # coil_sketch.py:61
+
+
+@dataclass
+class EngineResult:
+    x: torch.Tensor                 # (B, D) complex64, non-finite entries scrubbed
+    objectives: np.ndarray          # (T_run, B)
+    obj0: np.ndarray                # (B,)
+    diverged: np.ndarray            # (B,) bool
+    outer_run: np.ndarray           # (B,) outer iterations completed per slice
+    lipschitz: np.ndarray           # (B,)
+    counts: dict = field(default_factory=dict)
+    per_outer_counts: list = field(default_factory=list)
+    per_outer_wall: list = field(default_factory=list)
+    per_outer_dist: list = field(default_factory=list)
+
+
+class SketchedReconEngine:
+    """Device state of B slices sharing one grid, one Fourier kernel and one sketch design."""
+
+    def __init__(self, kernel, maps0: torch.Tensor, y: torch.Tensor, *, dims, sketch: SketchConfig,
+                 lam: float, reg: str = "l1-wavelet", solver: str = "fista", step_scale: float = 0.9,
+                 sqrt_w: torch.Tensor | None = None, wavelet_levels: int | None = None,
+                 counter: CostCounter | None = None):
+        self.kernel = kernel
+        self.maps0 = maps0.contiguous()          # (B, C0, D)
+        self.B, self.C0, self.D = self.maps0.shape
+        self.y = y.contiguous()                  # (B, C0, nmax) weighted measurements
+        self.sketch = sketch
+        self.lam = float(lam)
+        self.reg = reg
+        self.solver = solver
+        self.step_scale = float(step_scale)
+        self.sqrt_w = sqrt_w
+        self.dims = tuple(dims)
+        self.counter = counter if counter is not None else CostCounter()
+        self.dev = self.maps0.device
+        if reg not in ("l1-wavelet", "l2"):
+            raise NotImplementedError(f"regularizer {reg!r} is outside the hot-path scope")
+        if solver == "cg" and reg != "l2":
+            raise ValueError("cg sub-solver requires the l2 regularizer")
+        if solver not in ("fista", "cg"):
+            raise NotImplementedError(f"solver {solver!r} is outside the hot-path scope")
+        self.wav = WaveletEngine(self.dims, wavelet_levels, batch=self.B) if reg == "l1-wavelet" else None
+        B, D = self.B, self.D
+        mk = lambda: torch.zeros(B, D, dtype=torch.complex64, device=self.dev)  # noqa: E731
+        self.x, self.z, self.v, self.d, self.anchor = mk(), mk(), mk(), mk(), mk()
+        self.r = torch.zeros_like(self.y)
+        self.nparts = 64
+        self.partial = torch.zeros(B, self.C0, self.nparts, dtype=torch.float64, device=self.dev)
+        self.step = None       # (B,) float64 device
+        self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
+
+    # ------------------------------------------------------------ pieces
+    def _normal(self, maps, x, out, **kw):
+        return self.kernel.normal(maps, x, out, w=self.sqrt_w, **kw)
+
+    def objective(self, x) -> torch.Tensor:
+        """Per-slice 0.5||A x - y||^2 + g(x) (float64 device); leaves A x - y in self.r."""
+        self.kernel.forward(self.maps0, x, self.r, ymeas=self.y, partial=self.partial,
+                            partial_blocks=self.nparts, w=self.sqrt_w)
+        obj = 0.5 * self.partial.sum(dim=(1, 2))
+        if self.lam != 0.0:
+            if self.reg == "l1-wavelet":
+                obj = obj + self.lam * self.wav.l1_norm(x)
+            else:
+                obj = obj + 0.5 * self.lam * _norm2(x)
+        return obj
+
+    def true_gradient(self, out):
+        """d = A^H r with r = A x - y from the last objective (coil_sketch.py:123-126)."""
+        self.counter.add("coil_transform", 2 * self.C0)
+        self.kernel.adjoint(self.maps0, self.r, out, w=self.sqrt_w)
+        return out
+
+    def power_lambda(self, smaps, iters: int = 30, seed: int = 0) -> torch.Tensor:
+        """lambda_max(A_s^H A_s) per slice (linops.py:766-782), counters paused."""
+        g = seed_stream(seed, 0)
+        v0 = g.standard_normal(self.D) + 1j * g.standard_normal(self.D)
+        v0 = v0 / np.linalg.norm(v0)
+        v = dv.c64(np.broadcast_to(v0, (self.B, self.D)))
+        w = torch.empty_like(v)
+        nparts = _lib.lib().sr_reduce_nparts()
+        part = torch.empty(self.B, nparts, 2, dtype=torch.float64, device=self.dev)
+        r0 = torch.empty(self.B, 2, dtype=torch.float64, device=self.dev)
+        r1 = torch.empty_like(r0)
+        lam = torch.zeros(self.B, dtype=torch.float64, device=self.dev)
+        coef = torch.zeros(self.B, 4, dtype=torch.float32, device=self.dev)
+        flags = torch.zeros(self.B, dtype=torch.int32, device=self.dev)
+        st = dv.stream()
+        for _ in range(int(iters)):
+            self._normal(smaps, v, w)
+            _lib.call("sr_reduce", 0, dv.ptr(w), None, self.D, self.D, self.B, dv.ptr(part), dv.ptr(r0), st)
+            _lib.call("sr_reduce", 1, dv.ptr(v), dv.ptr(w), self.D, self.D, self.B, dv.ptr(part), dv.ptr(r1), st)
+            _lib.call("sr_scalar_op", 0, dv.ptr(r0), dv.ptr(r1), dv.ptr(lam), dv.ptr(coef), None,
+                      dv.ptr(flags), self.B, st)
+            _lib.call("sr_lincomb", dv.ptr(v), dv.ptr(w), None, None, dv.ptr(coef), 0.0, 0.0, 0.0,
+                      self.D, self.D, self.B, st)
+        return lam
+
+    def _fista(self, smaps, inner: int):
+        """Warm-started FISTA on the anchored sub-problem (coil_sketch.py:192-199, solvers.py:284-301)."""
+        self.x.copy_(self.anchor)
+        self.z.copy_(self.anchor)
+        t_k = 1.0
+        for _ in range(inner):
+            self.counter.add("coil_transform", 2 * smaps.shape[1])
+            # v = z - step * (A_s^H A_s (z - anchor) + d)
+            self._normal(smaps, self.z, self.v, anchor=self.anchor, coef=self.fcoef, u=self.z, d=self.d)
+            t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_k * t_k))
+            beta = (t_k - 1.0) / t_next
+            if self.reg == "l1-wavelet":
+                if self.lam == 0.0:
+                    _lincomb(self.z, self.v, self.x, None, 1.0 + beta, -beta, 0.0, self.B, self.D)
+                    self.x.copy_(self.v)
+                else:
+                    self.wav.prox(self.v, self.x, thresh=self.thresh, zout=self.z, xold=self.x, beta=beta)
+            else:  # l2 prox v / (1 + step lam), then momentum
+                _lincomb(self.v, self.v, None, None, 1.0, 0.0, 0.0, self.B, self.D, coef=self.l2coef)
+                _lincomb(self.z, self.v, self.x, None, 1.0 + beta, -beta, 0.0, self.B, self.D)
+                self.x.copy_(self.v)
+            t_k = t_next
+
+    def _cg(self, smaps, inner: int):
+        """(A_s^H A_s + lam I) delta = -d - lam x^t, x = x^t + delta (coil_sketch.py:182-191)."""
+        B, D, st = self.B, self.D, dv.stream()
+        delta = torch.zeros_like(self.x)
+        r = torch.empty_like(self.x)
+        _lincomb(r, self.d, self.anchor, None, -1.0, -self.lam, 0.0, B, D)
+        p = r.clone()
+        mp = torch.empty_like(r)
+        nparts = _lib.lib().sr_reduce_nparts()
+        part = torch.empty(B, nparts, 2, dtype=torch.float64, device=self.dev)
+        rs = torch.empty(B, 2, dtype=torch.float64, device=self.dev)
+        den = torch.empty_like(rs)
+        state = torch.zeros(B, 2, dtype=torch.float64, device=self.dev)
+        cA = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        cB = torch.zeros_like(cA)
+        _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
+        state[:, 0] = rs[:, 0]
+        state[:, 1] = (rs[:, 0] > 0).to(torch.float64)  # sqrt(rs) <= 0 stops at once
+        lcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        lcoef[:, 0] = 1.0
+        lcoef[:, 1] = self.lam
+        for _ in range(inner):
+            self.counter.add("coil_transform", 2 * smaps.shape[1])
+            self._normal(smaps, p, mp, coef=lcoef, u=p)
+            _lib.call("sr_reduce", 1, dv.ptr(p), dv.ptr(mp), D, D, B, dv.ptr(part), dv.ptr(den), st)
+            _lib.call("sr_scalar_op", 1, None, dv.ptr(den), dv.ptr(state), dv.ptr(cA), dv.ptr(cB), None, B, st)
+            _lib.call("sr_lincomb", dv.ptr(delta), dv.ptr(delta), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
+            _lib.call("sr_lincomb", dv.ptr(r), dv.ptr(r), dv.ptr(mp), None, dv.ptr(cB), 0, 0, 0, D, D, B, st)
+            _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
+            _lib.call("sr_scalar_op", 2, dv.ptr(rs), None, dv.ptr(state), dv.ptr(cA), None, None, B, st)
+            _lib.call("sr_lincomb", dv.ptr(p), dv.ptr(r), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
+        _lincomb(self.x, self.anchor, delta, None, 1.0, 1.0, 0.0, B, D)
+
+    # ------------------------------------------------------------ Algorithm 1
+    def run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
+            x_ref: torch.Tensor | None = None) -> EngineResult:
+        B = self.B
+        t_start = time.perf_counter()
+        if x0 is not None:
+            self.x.copy_(x0)
+        else:
+            self.x.zero_()
+        obj0 = self.objective(self.x).cpu().numpy()
+        alive = np.ones(B, dtype=bool)
+        diverged = np.zeros(B, dtype=bool)
+        outer_run = np.zeros(B, dtype=np.int64)
+        frozen = self.x.clone()
+        objs, cnts, walls, dists = [], [], [], []
+        lip = None
+        ref_norm = None
+        if x_ref is not None:
+            ref_norm = torch.linalg.vector_norm(x_ref.to(torch.complex128), dim=1).cpu().numpy()
+        for t in range(1, outer + 1):
+            self.true_gradient(self.d)
+            sk = gen_sketch_matrix(self.sketch.with_seed(child_seed(self.sketch.seed, t)), self.C0)
+            smaps = coil_contract(self.maps0, sk.mat)
+            if self.solver == "fista" and lip is None:
+                lam_max = self.power_lambda(smaps)
+                lip = lam_max / self.step_scale
+                step = 1.0 / lip
+                self.fcoef[:, 0] = (-step).float()
+                self.fcoef[:, 1] = 1.0
+                self.fcoef[:, 2] = (-step).float()
+                self.thresh.copy_((step * self.lam).float())
+                if self.reg == "l2":
+                    self.l2coef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+                    self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
+            self.anchor.copy_(self.x)
+            if self.solver == "fista":
+                self._fista(smaps, inner)
+            else:
+                self._cg(smaps, inner)
+            finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1).cpu().numpy()
+            obj = self.objective(self.x).cpu().numpy()
+            obj = np.where(finite, obj, np.inf)
+            objs.append(obj)
+            cnts.append(self.counter.value("coil_transform"))
+            walls.append(time.perf_counter() - t_start)
+            if x_ref is not None:
+                dd = torch.linalg.vector_norm((self.x - x_ref).to(torch.complex128), dim=1).cpu().numpy()
+                dists.append(dd / ref_norm)
+            else:
+                dists.append(np.full(B, np.nan))
+            newly = alive & ((~finite) | (obj > DIVERGENCE_FACTOR * obj0))
+            outer_run[alive] = t
+            if newly.any():
+                idx = torch.as_tensor(np.nonzero(newly)[0], device=self.dev)
+                frozen.index_copy_(0, idx, self.x.index_select(0, idx))
+                diverged |= newly
+                alive &= ~newly
+            if not alive.any():
+                break
+        x = self.x.clone()
+        if diverged.any():
+            idx = torch.as_tensor(np.nonzero(diverged)[0], device=self.dev)
+            x.index_copy_(0, idx, frozen.index_select(0, idx))
+        xr = torch.view_as_real(x)
+        x = torch.view_as_complex(torch.where(torch.isfinite(xr), xr, torch.zeros_like(xr)).contiguous())
+        return EngineResult(x, np.array(objs), obj0, diverged, outer_run,
+                            np.full(B, np.nan) if lip is None else lip.cpu().numpy(),
+                            self.counter.asdict(), cnts, walls, dists)
+
+
+def _norm2(x) -> torch.Tensor:
+    B, D = x.shape
+    nparts = _lib.lib().sr_reduce_nparts()
+    part = torch.empty(B, nparts, 2, dtype=torch.float64, device=x.device)
+    res = torch.empty(B, 2, dtype=torch.float64, device=x.device)
+    _lib.call("sr_reduce", 0, dv.ptr(x), None, D, D, B, dv.ptr(part), dv.ptr(res), dv.stream())
+    return res[:, 0]
+
+
+def _lincomb(out, X, Y, Z, cx, cy, cz, B, D, coef=None):
+    _lib.call("sr_lincomb", dv.ptr(out), dv.ptr(X), dv.ptr(Y), dv.ptr(Z), dv.ptr(coef), float(cx),
+              float(cy), float(cz), D, D, B, dv.stream())

@@ -1,0 +1,122 @@
+"""Device Daubechies-4 wavelet engine (K6): analysis, synthesis, fused L1 prox.
+
+Reference: WaveletOp (linops.py:654-702), default_wavelet_levels
+(linops.py:609-616), Regularizer.prox / value (solvers.py:61-81), prox_l1
+(solvers.py:129-135).  2-D grids (the image grids of every BASELINE config).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _device as dv
+from . import _lib
+
+
+def default_wavelet_levels(dims, cap: int = 4) -> int:
+    """Largest level count <= cap with every dim halvable (linops.py:609-616)."""
+    levels, d = 0, [int(n) for n in dims]
+    while levels < cap and all(n % 2 == 0 and n // 2 >= 1 for n in d):
+        d = [n // 2 for n in d]
+        levels += 1
+    return levels
+
+
+class WaveletEngine:
+    """Batched (B, ny, nx) multilevel DB4 on the device."""
+
+    def __init__(self, dims, levels: int | None = None, batch: int = 1):
+        dims = tuple(int(n) for n in dims)
+        if len(dims) != 2:
+            raise NotImplementedError("device wavelet implements 2-D grids")
+        if levels is None:
+            levels = default_wavelet_levels(dims)
+        levels = int(levels)
+        if levels < 1:
+            raise ValueError("levels must be >= 1")
+        for n in dims:
+            if n % (1 << levels) != 0:
+                raise ValueError(f"grid dims {dims} not divisible by 2^{levels}")
+        self.dims, self.levels, self.batch = dims, levels, int(batch)
+        self.ny, self.nx = dims
+        self.D = self.ny * self.nx
+        self.device = dv.require_cuda()
+        self.buf = [torch.empty(self.batch, self.D, dtype=torch.complex64, device=self.device)
+                    for _ in range(2)]
+        self.nblocks = [_lib.lib().sr_wavelet_ana2_nblocks(self.ny >> l, self.nx >> l)
+                        for l in range(levels)]
+        self.l1part = torch.zeros(self.batch, sum(self.nblocks), dtype=torch.float64,
+                                  device=self.device)
+
+    def _region(self, l):
+        return self.ny >> l, self.nx >> l
+
+    def _ana(self, src, dst, l, thresh=None, hthresh=-1.0, l1=None):
+        h, w = self._region(l)
+        _lib.call("sr_wavelet_ana2", dv.ptr(src), dv.ptr(dst), h, w, self.nx, self.D, self.batch,
+                  dv.ptr(thresh), float(hthresh), int(l == self.levels - 1), dv.ptr(l1), dv.stream())
+
+    def _syn(self, src, dst, l, zout=None, xold=None, beta=0.0):
+        h, w = self._region(l)
+        _lib.call("sr_wavelet_syn2", dv.ptr(src), dv.ptr(dst), h, w, self.nx, self.D, self.batch,
+                  dv.ptr(zout), dv.ptr(xold), float(beta), dv.stream())
+
+    def _l1slice(self, l):
+        o = sum(self.nblocks[:l])
+        return self.l1part[:, o: o + self.nblocks[l]]
+
+    # ------------------------------------------------------------- hot path
+    def prox(self, v, out, thresh=None, hthresh=-1.0, zout=None, xold=None, beta=0.0):
+        """out = Psi^H soft(Psi v, t); optional z = out + beta (out - xold).
+
+        thresh: device (B,) float32 thresholds or None with host `hthresh`.
+        v must not alias out, self.buf.  out may alias xold.
+        """
+        src = v
+        for l in range(self.levels):
+            dst = self.buf[l % 2]
+            self._ana(src, dst, l, thresh, hthresh)
+            src = dst
+        for l in range(self.levels - 1, -1, -1):
+            dst = out if l == 0 else self.buf[(l - 1) % 2]
+            if l == 0:
+                self._syn(self.buf[0], dst, 0, zout, xold, beta)
+            else:
+                self._syn(self.buf[l % 2], dst, l)
+        return out
+
+    def l1_norm(self, x) -> torch.Tensor:
+        """sum |Psi x| per slice as a (B,) float64 device tensor (no host sync)."""
+        src = x
+        for l in range(self.levels):
+            dst = self.buf[l % 2]
+            self._ana(src, dst, l, None, -1.0, self._l1slice(l))
+            src = dst
+        return self.l1part.sum(dim=1)
+
+    # ------------------------------------------------- reference-layout API
+    def forward(self, x, out):
+        """Coefficients in the reference in-place [lo|hi] layout (linops.py:677-687)."""
+        self._ana(x, out, 0)
+        tmp = self.buf[0]
+        o3 = out.view(self.batch, self.ny, self.nx)
+        t3 = tmp.view(self.batch, self.ny, self.nx)
+        for l in range(1, self.levels):
+            h, w = self._region(l)
+            self._ana(out, tmp, l)
+            o3[:, :h, :w].copy_(t3[:, :h, :w])
+        return out
+
+    def adjoint(self, c, out):
+        """Inverse/adjoint (linops.py:689-702)."""
+        work = self.buf[1]
+        work.copy_(c)
+        tmp = self.buf[0]
+        w3 = work.view(self.batch, self.ny, self.nx)
+        t3 = tmp.view(self.batch, self.ny, self.nx)
+        for l in range(self.levels - 1, 0, -1):
+            h, w = self._region(l)
+            self._syn(work, tmp, l)
+            w3[:, :h, :w].copy_(t3[:, :h, :w])
+        self._syn(work, out, 0)
+        return out

@@ -1,0 +1,182 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and the
+reference's golden vectors.  Bars (BASELINE.json north_star): per-operator
+relative L2 <= 1e-4, final-image NRMSE <= 1e-3; integer/index work exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, rel
+from oracle import sketch_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-4      # per-operator relative L2 (north_star)
+IMG_TOL = 1e-3     # final-image NRMSE (north_star)
+
+
+def _api():
+    from paper_2305_06482_b200 import coil_sketch, forward_model, linops, sketching, solvers
+    return coil_sketch, forward_model, linops, sketching, solvers
+
+
+@pytest.mark.parametrize("name", ["sense_cart", "sense_cart_b", "sense_cart_1d"])
+def test_sense_operator_matches_reference(cuda, name):
+    cs, fm, lo, sk, so = _api()
+    g = golden(name)
+    shape = lo.GridShape(tuple(g["dims"]))
+    traj = lo.Trajectory(g["points"], "cartesian-mask")
+    a = fm.build_sense(fm.SensitivityMaps(shape, g["maps"]), traj)
+    assert rel(a.forward(g["x"]), g["Ax"]) < OP_TOL
+    assert rel(a.adjoint(g["y"]), g["AHy"]) < OP_TOL
+    assert rel(a.adjoint(a.forward(g["x"])), g["AHAx"]) < OP_TOL
+    S = sk.SketchMatrix(g["S"], sk.SketchConfig(3, 2, 1))
+    a_s = sk.build_sketched_operator(a, S)
+    assert rel(a_s.adjoint(a_s.forward(g["x"])), g["AsHAsx"]) < OP_TOL
+    # fused normal entry point
+    x = torch.from_numpy(g["x"].astype(np.complex64)).cuda().view(1, -1)
+    out = torch.empty_like(x)
+    a_s.normal_into(x, out)
+    assert rel(out.cpu().numpy().ravel(), g["AsHAsx"]) < OP_TOL
+    # V identity rows of the sketch are bit-exact copies of the (fp32) maps
+    np.testing.assert_array_equal(a_s.maps_dev[0, :2].cpu().numpy(), g["maps"][:2].astype(np.complex64))
+    lam = so.normal_max_eig(a_s)
+    assert abs(lam - float(g["lam_max"])) <= 1e-5 * float(g["lam_max"])
+    # counters: forward + adjoint + adjoint(forward) on the full op = 4C; sketched pair + fused normal
+    # = 2*3 + 2*3; the power iteration is paused (linops.py:774)
+    assert a.counts["coil_transform"] == 4 * a.n_coils + 12
+
+
+def test_kernel_plugin_protocol(cuda):
+    """The device kernel honours the reference plugin protocol (apply / apply_adjoint)."""
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    g = golden("sense_cart")
+    dims = tuple(g["dims"])
+    kern = CartesianKernel.from_points(dims, g["points"])
+    ok = O.CartesianKernel(dims, g["points"])
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal((4, int(np.prod(dims)))) + 1j * rng.standard_normal((4, int(np.prod(dims))))
+    yb = rng.standard_normal((4, ok.n_points)) + 1j * rng.standard_normal((4, ok.n_points))
+    assert kern.n_points == ok.n_points
+    assert rel(kern.apply(b), ok.apply(b)) < OP_TOL
+    assert rel(kern.apply_adjoint(yb), ok.apply_adjoint(yb)) < OP_TOL
+    # and plugged into the oracle's SENSE operator (the reference's seam, FM:134)
+    a = O.Sense(g["maps"], kern)
+    assert rel(a.normal(g["x"]), g["AHAx"]) < OP_TOL
+
+
+@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24"])
+def test_wavelet_and_prox(cuda, name):
+    cs, fm, lo, sk, so = _api()
+    g = golden(name)
+    shape = lo.GridShape(tuple(g["dims"]))
+    w = lo.WaveletOp(shape)
+    assert w.levels == int(g["levels"])
+    assert rel(w.forward(g["x"]), g["fwd"]) < OP_TOL
+    assert rel(w.adjoint(g["x"]), g["adj"]) < OP_TOL
+    reg = so.make_regularizer("l1-wavelet", 0.3, shape)
+    assert rel(reg.prox(g["x"], 0.7), g["prox"]) < OP_TOL
+    assert abs(reg.value(g["x"]) - float(g["value"])) < 1e-5 * float(g["value"])
+
+
+@pytest.mark.parametrize("dims", [(320, 320), (256, 256), (256, 160), (64, 40), (200, 80)])
+def test_batched_normal_op_vs_oracle(cuda, dims):
+    """K1 at BASELINE geometries (a few slices, per-slice masks and maps)."""
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    rng = np.random.default_rng(7)
+    B, C = 3, 5
+    D = dims[0] * dims[1]
+    plans, pts_all = [], []
+    for b in range(B):
+        m = rng.random(dims) < 0.2
+        pts = np.argwhere(m) - np.array([n // 2 for n in dims])
+        pts_all.append(pts)
+        plans.append(cartesian_plan(dims, pts))
+    kern = CartesianKernel(dims, plans)
+    maps = (rng.standard_normal((B, C, D)) + 1j * rng.standard_normal((B, C, D))) / 3
+    x = rng.standard_normal((B, D)) + 1j * rng.standard_normal((B, D))
+    md = torch.from_numpy(maps.astype(np.complex64)).cuda()
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    out = torch.empty_like(xd)
+    kern.normal(md, xd, out)
+    got = out.cpu().numpy()
+    for b in range(B):
+        ref = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b])).normal(x[b])
+        assert rel(got[b], ref) < OP_TOL, b
+    # forward / adjoint with ragged per-slice samples
+    y = kern.forward(md, xd)
+    for b in range(B):
+        a = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b]))
+        n = len(pts_all[b])
+        assert rel(y[b, :, :n].cpu().numpy().ravel(), a.forward(x[b])) < OP_TOL
+    adj = torch.empty_like(xd)
+    kern.adjoint(md, y, adj)
+    for b in range(B):
+        a = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b]))
+        n = len(pts_all[b])
+        assert rel(adj[b].cpu().numpy(), a.adjoint(y[b, :, :n].cpu().numpy().astype(np.complex128).ravel())) < OP_TOL
+
+
+def test_fused_fista_epilogue(cuda):
+    """out = z - step (N(z - a) + d) in one K1 call (coil_sketch.py:196-197, solvers.py:291)."""
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    g = golden("sense_cart_b")
+    dims = tuple(g["dims"])
+    kern = CartesianKernel.from_points(dims, g["points"])
+    rng = np.random.default_rng(3)
+    D = int(np.prod(dims))
+    z, a, d = (rng.standard_normal(D) + 1j * rng.standard_normal(D) for _ in range(3))
+    step = 0.37
+    ref = z - step * (O.Sense(g["maps"], O.CartesianKernel(dims, g["points"])).normal(z - a) + d)
+    t = lambda v: torch.from_numpy(v.astype(np.complex64)).cuda().view(1, -1)  # noqa: E731
+    coef = torch.tensor([[-step, 1.0, -step, 0.0]], dtype=torch.float32, device="cuda")
+    zt = t(z)
+    out = torch.empty_like(zt)
+    kern.normal(torch.from_numpy(g["maps"].astype(np.complex64)).cuda().unsqueeze(0), zt, out,
+                anchor=t(a), coef=coef, u=zt, d=t(d))
+    assert rel(out.cpu().numpy().ravel(), ref) < OP_TOL
+
+
+def test_reductions_are_deterministic(cuda):
+    from paper_2305_06482_b200.solvers import dev_norm2, dev_vdot
+    rng = np.random.default_rng(5)
+    a = torch.from_numpy((rng.standard_normal((4, 100003)) + 1j * rng.standard_normal((4, 100003))).astype(np.complex64)).cuda()
+    b = torch.roll(a, 1, dims=1).contiguous()
+    r1, r2 = dev_norm2(a).cpu().numpy(), dev_norm2(a).cpu().numpy()
+    np.testing.assert_array_equal(r1, r2)
+    np.testing.assert_array_equal(dev_vdot(a, b).cpu().numpy(), dev_vdot(a, b).cpu().numpy())
+    an = a.cpu().numpy().astype(np.complex128)
+    np.testing.assert_allclose(r1, np.sum(np.abs(an) ** 2, axis=1), rtol=1e-12)
+
+
+def _recon_inputs(g):
+    cs, fm, lo, sk, so = _api()
+    dims = tuple(int(n) for n in g["dims"])
+    shape = lo.GridShape(dims)
+    nufft = float(g["oversamp"]) > 0
+    traj = lo.Trajectory(g["points"], "non-cartesian" if nufft else "cartesian-mask")
+    return cs, fm, lo, sk, so, dims, shape, traj, nufft
+
+
+@pytest.mark.parametrize("name,solver,kind", [("recon_cart", "fista", "l1-wavelet"),
+                                              ("recon_cart_pm1", "fista", "l1-wavelet"),
+                                              ("recon_cart_cg", "cg", "l2")])
+def test_coil_sketching_recon_matches_reference(cuda, name, solver, kind):
+    g = golden(name)
+    cs, fm, lo, sk, so, dims, shape, traj, nufft = _recon_inputs(g)
+    reg = so.make_regularizer(kind, float(g["lam"]), shape)
+    v, s = int(g["v"]), int(g["s"])
+    cfg = cs.CoilSketchConfig(int(g["chat0"]), sk.SketchConfig(v + s, v, s, "rademacher", 0,
+                                                               rademacher_scale=float(g["scale"])),
+                              reg, int(g["outer"]), int(g["inner"]), solver=solver)
+    rep = cs.coil_sketching_recon(fm.KSpaceData(traj, g["data"]), fm.SensitivityMaps(shape, g["maps"]), cfg)
+    x = rep.x_final.values
+    ref = g["x_final"]
+    nrmse = np.linalg.norm(np.abs(x) - np.abs(ref)) / np.linalg.norm(ref)
+    assert nrmse <= IMG_TOL
+    assert rel(x, ref) <= IMG_TOL
+    np.testing.assert_allclose([r.objective for r in rep.per_outer], g["objectives"], rtol=1e-4)
+    assert rep.counts["coil_transform"] == int(g["counts"]) == int(g["expected"])
+    assert rep.diverged == bool(g["diverged"])

@@ -1,0 +1,94 @@
+"""CPU tests of the host side: C-ABI exports, perm-order layout tables.
+
+The kernels' data flow (perm-order spectrum, mask, sample gather/scatter with
+centering phases) is emulated here in numpy with the SAME host tables the GPU
+consumes, and compared with the oracle -- so a layout bug is caught without a GPU.
+"""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, rel
+from oracle import sketch_oracle as O
+from paper_2305_06482_b200 import _lib, plan
+
+
+def header_symbols():
+    text = (ROOT / "include" / "sketchrecon_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(?:int|long long)\s+(sr_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.exported_symbols())
+
+
+def test_fft_split_table():
+    for n in (256, 320, 160, 640, 200, 16, 20, 8):
+        p, q = _lib.fft_split(n)
+        assert p * q == n
+        pos = plan.perm_positions(n)
+        assert sorted(pos) == list(range(n))
+    with pytest.raises(ValueError):
+        _lib.fft_split(7 * 11)
+
+
+def _emulate(dims, points, maps, x, y):
+    pl = plan.cartesian_plan(dims, points)
+    ny, nx = plan.grid2d(dims)
+    D = ny * nx
+    maskpp = pl.maskT.reshape(nx, ny).T  # [pos_y, pos_x]
+    to_pp = lambda s: plan.to_perm_spectrum(s, ny, nx)  # noqa: E731
+    py = plan.perm_positions(ny) if ny > 1 else np.zeros(1, int)
+    px = plan.perm_positions(nx)
+    from_pp = lambda s: s[..., py[:, None], px[None, :]]  # noqa: E731
+    imgs = maps.reshape(-1, ny, nx) * x.reshape(ny, nx)
+    spec = to_pp(np.fft.fft2(imgs))
+    # forward: gather with phase, 1/sqrt(D)
+    fwd = (spec.reshape(len(maps), -1)[:, pl.spos] * pl.ph) / np.sqrt(D)
+    # normal: mask / D, inverse, conj coil sum
+    nrm = np.fft.ifft2(from_pp(spec * maskpp / D)) * D
+    nrm = np.sum(np.conj(maps.reshape(-1, ny, nx)) * nrm, axis=0).ravel()
+    # adjoint: scatter (write list), conj phase, 1/sqrt(D)
+    sp = np.zeros((len(maps), D), complex)
+    yy = y.reshape(len(maps), -1)
+    sp[:, pl.spos[pl.wlist]] = yy[:, pl.wlist] * np.conj(pl.ph[pl.wlist]) / np.sqrt(D)
+    adj = np.fft.ifft2(from_pp(sp.reshape(-1, ny, nx))) * D
+    adj = np.sum(np.conj(maps.reshape(-1, ny, nx)) * adj, axis=0).ravel()
+    return fwd.ravel(), nrm, adj
+
+
+@pytest.mark.parametrize("name", ["sense_cart", "sense_cart_b", "sense_cart_1d"])
+def test_perm_layout_emulation_matches_reference(name):
+    g = golden(name)
+    dims = tuple(int(n) for n in g["dims"])
+    fwd, nrm, adj = _emulate(dims, g["points"], g["maps"], g["x"], g["y"])
+    assert rel(fwd, g["Ax"]) < 1e-12
+    assert rel(nrm, g["AHAx"]) < 1e-12
+    assert rel(adj, g["AHy"]) < 1e-12
+
+
+def test_duplicate_bins_last_write_wins():
+    pts = np.array([[0, 0], [1, 2], [0, 0], [-3, 1], [1, 2]], float)
+    pl = plan.cartesian_plan((8, 8), pts)
+    assert list(pl.wlist) == [2, 3, 4]
+    assert pl.maskT.sum() == 3
+
+
+def test_oracle_kernel_parity_small():
+    # oracle self-consistency: adjointness of the Cartesian SENSE operator
+    rng = np.random.default_rng(1)
+    dims = (16, 12)
+    pts = np.argwhere(rng.random(dims) < 0.4) - np.array([8, 6])
+    maps = rng.standard_normal((3, 192)) + 1j * rng.standard_normal((3, 192))
+    a = O.Sense(maps, O.CartesianKernel(dims, pts))
+    u = rng.standard_normal(192) + 1j * rng.standard_normal(192)
+    v = rng.standard_normal(3 * len(pts)) + 1j * rng.standard_normal(3 * len(pts))
+    assert abs(np.vdot(v, a.forward(u)) - np.vdot(a.adjoint(v), u)) < 1e-10 * np.linalg.norm(u) * np.linalg.norm(v)
