@@ -52,11 +52,14 @@ int sr_fft_split(int n, int* P, int* Q);
  *   ws: workspace of batch*ncoils*ny*nx complex64
  *   anchor: NULL or (batch, ny, nx): operator input is x - anchor
  *   coef: NULL -> out = acc; else device float4 per slice {s_acc, s_u, s_d, -}:
- *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v) */
+ *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v)
+ *   chunk: slices per pass group (0 = all): the three passes run per group of
+ *          `chunk` slices so the coil workspace (chunk*ncoils*ny*nx) stays L2-resident */
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
-                   const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+                   const float* coef, const sr_c64* u, const sr_c64* d, int chunk,
+                   void* stream);
 
 /* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
  * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)

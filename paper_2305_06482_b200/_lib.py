@@ -21,7 +21,7 @@ _f = C.c_float
 SIGNATURES = {
     "sr_fft_size_supported": [_i],
     "sr_fft_split": [_i, C.POINTER(_i), C.POINTER(_i)],
-    "sr_cart_normal": [_vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp],
+    "sr_cart_normal": [_vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
     "sr_cart_forward": [_vp, _vp, _ll, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp],
     "sr_cart_adjoint": [_vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
                         _vp, _vp, _vp, _vp],

@@ -59,6 +59,7 @@ class CartesianKernel:
         woff[1:] = np.cumsum([len(p.wlist) for p in per_slice])
         self.woff = dv.host_to_dev(woff, torch.int64, dev)
         self._ws = None
+        self.chunk = 0  # slices per pass group of the fused normal op (0 = whole batch)
         self._plans = plans
         self._replicas: dict[int, "CartesianKernel"] = {}
 
@@ -87,16 +88,21 @@ class CartesianKernel:
         if t.shape != (self.batch, self.D) or t.dtype != torch.complex64 or not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous complex64 ({self.batch}, {self.D})")
 
-    def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None):
-        """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1)."""
+    def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None, chunk=None):
+        """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1).
+
+        chunk: slices per pass group (None -> self.chunk; 0 -> all at once).
+        """
         _no_weights(w)
         ncoils, mbs = self._maps_stride(maps)
         for t, n in ((x, "x"), (out, "out"), (anchor, "anchor"), (u, "u"), (d, "d")):
             self._check_img(t, n)
-        ws = self.workspace(ncoils)
+        chunk = self.chunk if chunk is None else int(chunk)
+        chunk = self.batch if chunk <= 0 else min(chunk, self.batch)
+        ws = self.workspace(ncoils, chunk)
         _lib.call("sr_cart_normal", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), mbs,
                   dv.ptr(self.maskT), self.mask_bstride, dv.ptr(out), dv.ptr(ws), self.batch,
-                  ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), dv.stream())
+                  ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), chunk, dv.stream())
         return out
 
     def forward(self, maps, x, y=None, *, ymeas=None, partial=None, partial_blocks=64, w=None):

@@ -21,21 +21,27 @@
 namespace {
 
 // ------------------------------------------------------------------- pass A
+constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+
+// ROWS rows per CTA, one thread per (row, p): T = ROWS * P is a whole number
+// of warps and at least 128 threads.
 template <int P, int Q>
 struct RowCfg {
-  static constexpr int ROWS = (P >= 128) ? 1 : (128 / P > 64 ? 64 : 128 / P);
+  static constexpr int BASE = 32 / cgcd(P, 32);
+  static constexpr int ROWS = BASE * ((128 / (BASE * P)) > 1 ? (128 / (BASE * P)) : 1);
   static constexpr int T = ROWS * P;
+  static constexpr int MINB = (T <= 128) ? 4 : 3;
 };
 
 template <int P, int Q>
-__global__ void __launch_bounds__(RowCfg<P, Q>::T)
+__global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          const float2* __restrict__ maps, float2* __restrict__ ws,
          int ncoils, int ny, long long x_bstride, long long map_bstride) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
-  __shared__ float2 tw[N];
-  __shared__ float2 buf[ROWS * S::VS];
+  __shared__ float2 t1[N];
+  __shared__ __align__(16) float2 buf[ROWS * S::VS];
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
@@ -43,32 +49,33 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   const int row = row0 + lr;
   const bool valid = row < ny;
   const long long D = (long long)ny * N;
-  init_twiddles<N>(tw, tid, T);
-
-  float2 xv[Q];
+  init_tw_s1<P, Q>(t1, tid, T);
+  __syncthreads();
   const float2* xr = x + b * x_bstride + (long long)row * N + p;
   const float2* ar = anchor ? anchor + b * x_bstride + (long long)row * N + p : nullptr;
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    float2 v = valid ? xr[P * q] : make_float2(0.f, 0.f);
-    if (ar && valid) v = csub(v, ar[P * q]);
-    xv[q] = v;
-  }
-  __syncthreads();
-  const float2* mb = maps + b * map_bstride;
-  float2* wb = ws + (long long)b * ncoils * D;
+  const float2* mb = maps + b * map_bstride + (long long)row * N + p;
+  float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
+  const int nvalid = min(ROWS, ny - row0) * N;
   for (int j = 0; j < ncoils; ++j) {
     float2 r[Q];
-    const float2* mr = mb + j * D + (long long)row * N + p;
+    const float2* mr = mb + j * D;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) r[q] = valid ? cmul(__ldg(mr + P * q), xv[q]) : make_float2(0.f, 0.f);
-    fft_s1_fwd<P, Q>(r, p, tw);
+    for (int q = 0; q < Q; ++q) {
+      float2 v = make_float2(0.f, 0.f);
+      if (valid) {
+        v = __ldg(xr + P * q);
+        if (ar) v = csub(v, __ldg(ar + P * q));
+        v = cmul(__ldg(mr + P * q), v);
+      }
+      r[q] = v;
+    }
+    fft_s1_fwd<P, Q>(r, p, t1);
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
     __syncthreads();
     if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
-        const int l2 = it / Q, k2 = it % Q;
+        const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
         float2* gp = buf + l2 * S::VS + S::GS * k2;
 #pragma unroll
@@ -79,8 +86,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
       }
       __syncthreads();
     }
-    float2* wj = wb + j * D + (long long)row0 * N;
-    const int nvalid = min(ROWS, ny - row0) * N;
+    float2* wj = wb + j * D;
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
       wj[e] = buf[l3 * S::VS + S::pad(pos)];
@@ -93,15 +99,15 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
 // Epilogue: out = s_acc * acc + s_u * u + s_d * d, coefficients per slice
 // (coef[b] = {s_acc, s_u, s_d, unused}); coef == nullptr -> out = acc.
 template <int P, int Q>
-__global__ void __launch_bounds__(RowCfg<P, Q>::T)
+__global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
          const float2* __restrict__ u, const float2* __restrict__ d) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
-  __shared__ float2 tw[N];
-  __shared__ float2 buf[ROWS * S::VS];
+  __shared__ float2 t2[N];
+  __shared__ __align__(16) float2 buf[ROWS * S::VS];
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
@@ -109,15 +115,15 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   const int row = row0 + lr;
   const bool valid = row < ny;
   const long long D = (long long)ny * N;
-  init_twiddles<N>(tw, tid, T);
+  init_tw_s2<P, Q>(t2, tid, T);
   float2 acc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = make_float2(0.f, 0.f);
-  const float2* mb = maps + b * map_bstride;
-  const float2* wb = ws + (long long)b * ncoils * D;
+  const float2* mb = maps + b * map_bstride + (long long)row * N + p;
+  const float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   const int nvalid = min(ROWS, ny - row0) * N;
   for (int j = 0; j < ncoils; ++j) {
-    const float2* wj = wb + j * D + (long long)row0 * N;
+    const float2* wj = wb + j * D;
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
       buf[l3 * S::VS + S::pad(pos)] = wj[e];
@@ -125,12 +131,12 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
     __syncthreads();
     if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
-        const int l2 = it / Q, k2 = it % Q;
+        const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
         float2* gp = buf + l2 * S::VS + S::GS * k2;
 #pragma unroll
         for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-        fft_s2_inv<P, Q>(g, k2, tw);
+        fft_s2_inv<P, Q>(g, k2, t2);
 #pragma unroll
         for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
       }
@@ -141,7 +147,7 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
     for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[lr * S::VS + S::GS * k2 + p];
     fft_s1_inv<Q>(r);
     if (valid) {
-      const float2* mr = mb + j * D + (long long)row * N + p;
+      const float2* mr = mb + j * D;
 #pragma unroll
       for (int q = 0; q < Q; ++q) cfma_conj(acc[q], __ldg(mr + P * q), r[q]);
     }
@@ -171,7 +177,7 @@ template <int P, int Q>
 struct ColCfg {
   static constexpr int CB = (P >= 16) ? 16 : (P >= 4 ? 32 : 64);
   static constexpr int T = CB * P;
-  static constexpr int VSP = FftShape<P, Q>::VS | 1;  // odd stride: conflict-free over columns
+  static constexpr int VSP = FftShape<P, Q>::VS0 | 1;  // odd stride: conflict-free over columns
 };
 
 template <int P, int Q>
@@ -181,15 +187,17 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
   using S = FftShape<P, Q>;
   constexpr int N = S::N, CB = ColCfg<P, Q>::CB, T = ColCfg<P, Q>::T, VSP = ColCfg<P, Q>::VSP;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* buf = smem + N;
+  float2* t1 = smem;
+  float2* t2 = smem + N;
+  float2* buf = smem + 2 * N;
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * CB;
   const int j = blockIdx.y, b = blockIdx.z;
   const long long D = (long long)nx * N;
   float2* img = ws + ((long long)b * ncoils + j) * D;
   const int ncols = min(CB, nx - c0);
-  init_twiddles<N>(tw, tid, T);
+  init_tw_s1<P, Q>(t1, tid, T);
+  init_tw_s2<P, Q>(t2, tid, T);
   __syncthreads();
   const int c = tid % CB, p = tid / CB;
   const bool cvalid = c < ncols;
@@ -207,7 +215,7 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
 #pragma unroll
     for (int q = 0; q < Q; ++q)
       r[q] = cvalid ? img[(long long)(p + P * q) * nx + c0 + c] : make_float2(0.f, 0.f);
-    fft_s1_fwd<P, Q>(r, p, tw);
+    fft_s1_fwd<P, Q>(r, p, t1);
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[c * VSP + S::GS * k2 + p] = r[k2];
     __syncthreads();
@@ -225,10 +233,20 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
     if (mode != COL_INV) fft_s2_fwd<P>(g);
     if (mode == COL_NORMAL) {
       const uint8_t* mk = mcol + (long long)(c0 + cc) * N + P * k2;
+      if ((P % 4) == 0) {
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mk[k1] ? mscale : 0.f);
+        for (int w4 = 0; w4 < P / 4; ++w4) {
+          const uint32_t m4 = __ldg(reinterpret_cast<const uint32_t*>(mk) + w4);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            g[4 * w4 + i] = cscale(g[4 * w4 + i], ((m4 >> (8 * i)) & 0xffu) ? mscale : 0.f);
+        }
+      } else {
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mk[k1] ? mscale : 0.f);
+      }
     }
-    if (mode != COL_FWD) fft_s2_inv<P, Q>(g, k2, tw);
+    if (mode != COL_FWD) fft_s2_inv<P, Q>(g, k2, t2);
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
   }
@@ -331,7 +349,7 @@ template <int P, int Q>
 int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
                    int batch, int ncoils, int nx, cudaStream_t st) {
   using C = ColCfg<P, Q>;
-  const size_t smem = sizeof(float2) * (P * Q + C::CB * C::VSP);
+  const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(k_colpass<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -412,20 +430,32 @@ int sr_fft_split(int n, int* P, int* Q) {
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
-                   const float* coef, const sr_c64* u, const sr_c64* d, void* stream) {
-  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2) return SR_EINVAL;
+                   const float* coef, const sr_c64* u, const sr_c64* d, int chunk, void* stream) {
+  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < 0) return SR_EINVAL;
   if (!fft_size_supported(nx) || !fft_size_supported(ny)) return SR_EUNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
   const long long D = (long long)ny * nx;
-  int rc = dispatch_rowfwd(nx, (const float2*)x, (const float2*)anchor, (const float2*)maps,
-                           (float2*)ws, batch, ncoils, ny, D, map_bstride, st);
-  if (rc) return rc;
-  rc = dispatch_colpass(ny, (float2*)ws, maskT, mask_bstride, (float)(1.0 / (double)D),
-                        COL_NORMAL, batch, ncoils, nx, st);
-  if (rc) return rc;
-  return dispatch_rowinv(nx, (const float2*)ws, (const float2*)maps, (float2*)out, batch,
-                         ncoils, ny, D, map_bstride, (const float4*)coef, (const float2*)u,
-                         (const float2*)d, st);
+  if (chunk == 0 || chunk > batch) chunk = batch;
+  for (int b0 = 0; b0 < batch; b0 += chunk) {
+    const int nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+    const long long xo = (long long)b0 * D;
+    const float2* xc = (const float2*)x + xo;
+    const float2* ac = anchor ? (const float2*)anchor + xo : nullptr;
+    const float2* mc = (const float2*)maps + (long long)b0 * map_bstride;
+    const uint8_t* kc = maskT + (long long)b0 * mask_bstride;
+    float2* oc = (float2*)out + xo;
+    const float4* cc = coef ? (const float4*)coef + b0 : nullptr;
+    const float2* uc = u ? (const float2*)u + xo : nullptr;
+    const float2* dc = d ? (const float2*)d + xo : nullptr;
+    int rc = dispatch_rowfwd(nx, xc, ac, mc, (float2*)ws, nb, ncoils, ny, D, map_bstride, st);
+    if (rc) return rc;
+    rc = dispatch_colpass(ny, (float2*)ws, kc, mask_bstride, (float)(1.0 / (double)D), COL_NORMAL,
+                          nb, ncoils, nx, st);
+    if (rc) return rc;
+    rc = dispatch_rowinv(nx, (const float2*)ws, mc, oc, nb, ncoils, ny, D, map_bstride, cc, uc, dc, st);
+    if (rc) return rc;
+  }
+  return SR_OK;
 }
 
 int sr_cart_forward(const sr_c64* x, const sr_c64* maps, long long map_bstride,

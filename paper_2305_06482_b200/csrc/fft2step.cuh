@@ -28,29 +28,46 @@ struct FftShape {
   static constexpr int Q = Q_;
   static constexpr int N = P_ * Q_;
   static constexpr int GS = (P_ == 1) ? 1 : P_ + 1;  // padded group stride
-  static constexpr int VS = Q_ * GS;                  // padded vector length
+  // padded vector stride, VS = P (mod 16): rows of a CTA then interleave in the
+  // 32 banks exactly like contiguous data (conflict-free step-1 stores)
+  static constexpr int VS0 = Q_ * GS;
+  static constexpr int VS = VS0 + ((((P_ % 16) - (VS0 % 16)) % 16 + 16) % 16);
   __device__ __forceinline__ static int pad(int pos) { return (P_ == 1) ? pos : pos + pos / P_; }
   // perm position of frequency k (forward output layout)
   __host__ __device__ __forceinline__ static int perm_pos(int k) { return P_ * (k % Q_) + k / Q_; }
 };
 
-// tw[m] = exp(-2 pi i m / N), m in [0, N): double-precision sincospi, rounded once.
-template <int N>
-__device__ __forceinline__ void init_twiddles(float2* tw, int tid, int nthreads) {
-  for (int m = tid; m < N; m += nthreads) {
+// Twiddle tables, double-precision sincospi rounded once to float:
+//   t1[k2*P + p] = W_N^{p k2}   (forward step 1; lanes vary p  -> conflict-free)
+//   t2[m1*Q + k2] = W_N^{m1 k2} (inverse step 2'; lanes vary k2 -> conflict-free)
+template <int P, int Q>
+__device__ __forceinline__ void init_tw_s1(float2* t1, int tid, int nthreads) {
+  constexpr int N = P * Q;
+  for (int e = tid; e < N; e += nthreads) {
+    const int k2 = e / P, p = e - k2 * P;
     double s, c;
-    sincospi(-2.0 * (double)m / (double)N, &s, &c);
-    tw[m] = make_float2((float)c, (float)s);
+    sincospi(-2.0 * (double)(p * k2) / (double)N, &s, &c);
+    t1[e] = make_float2((float)c, (float)s);
+  }
+}
+template <int P, int Q>
+__device__ __forceinline__ void init_tw_s2(float2* t2, int tid, int nthreads) {
+  constexpr int N = P * Q;
+  for (int e = tid; e < N; e += nthreads) {
+    const int m1 = e / Q, k2 = e - m1 * Q;
+    double s, c;
+    sincospi(-2.0 * (double)(m1 * k2) / (double)N, &s, &c);
+    t2[e] = make_float2((float)c, (float)s);
   }
 }
 
 // forward step 1: r[q] = x[p + P q]  ->  r[k2] = W_N^{p k2} * DFT_Q(r)[k2]
 template <int P, int Q>
-__device__ __forceinline__ void fft_s1_fwd(float2* r, int p, const float2* tw) {
+__device__ __forceinline__ void fft_s1_fwd(float2* r, int p, const float2* t1) {
   RegDFT<Q, false>::run(r);
   if (P > 1) {
 #pragma unroll
-    for (int k2 = 1; k2 < Q; ++k2) r[k2] = cmul(r[k2], tw[p * k2]);
+    for (int k2 = 1; k2 < Q; ++k2) r[k2] = cmul(r[k2], t1[k2 * P + p]);
   }
 }
 
@@ -60,11 +77,11 @@ __device__ __forceinline__ void fft_s2_fwd(float2* g) { RegDFT<P, false>::run(g)
 
 // inverse step 2': group (index k1) -> IDFT_P (index m1), then *= conj(W_N^{m1 k2})
 template <int P, int Q>
-__device__ __forceinline__ void fft_s2_inv(float2* g, int k2, const float2* tw) {
+__device__ __forceinline__ void fft_s2_inv(float2* g, int k2, const float2* t2) {
   RegDFT<P, true>::run(g);
   if (Q > 1) {
 #pragma unroll
-    for (int m1 = 1; m1 < P; ++m1) g[m1] = cmulc(tw[m1 * k2], g[m1]);
+    for (int m1 = 1; m1 < P; ++m1) g[m1] = cmulc(t2[m1 * Q + k2], g[m1]);
   }
 }
 
@@ -77,8 +94,8 @@ __device__ __forceinline__ void fft_s1_inv(float2* r) { RegDFT<Q, true>::run(r);
 #define SR_FFT_SIZES(X)                                                          \
   X(1, 1, 1) X(2, 1, 2) X(3, 1, 3) X(4, 1, 4) X(5, 1, 5) X(6, 1, 6) X(8, 1, 8)             \
   X(10, 1, 10) X(12, 1, 12) X(16, 1, 16) X(20, 1, 20) X(24, 1, 24) X(25, 1, 25) \
-  X(32, 16, 2) X(40, 8, 5) X(48, 16, 3) X(50, 2, 25) X(64, 16, 4)               \
-  X(80, 16, 5) X(96, 16, 6) X(100, 4, 25) X(128, 16, 8) X(160, 16, 10)          \
-  X(192, 16, 12) X(200, 8, 25) X(256, 16, 16) X(320, 16, 20) X(384, 16, 24)     \
-  X(400, 16, 25) X(512, 16, 32) X(640, 32, 20) X(768, 32, 24) X(800, 32, 25)    \
+  X(32, 16, 2) X(40, 8, 5) X(48, 16, 3) X(50, 10, 5) X(64, 16, 4)              \
+  X(80, 16, 5) X(96, 16, 6) X(100, 10, 10) X(128, 16, 8) X(160, 16, 10)         \
+  X(192, 16, 12) X(200, 20, 10) X(256, 16, 16) X(320, 20, 16) X(384, 24, 16)    \
+  X(400, 20, 20) X(512, 32, 16) X(640, 32, 20) X(768, 32, 24) X(800, 32, 25)    \
   X(1024, 32, 32)

@@ -1,0 +1,38 @@
+#!/usr/bin/env python3
+"""Sweep K1 (fused Cartesian normal op) settings on the config-1 workload.
+
+Prints one line per setting with ms/apply and algorithmic GB/s.  Used to pick
+the slice-chunk size (L2 residency of the coil workspace); not part of bench.
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--chunks", default="0,32,16,8,4,2,1")
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    w = bench.build_workload(0, dev)
+    kern, smaps, x = w["kern"], w["smaps"], w["x"]
+    out = torch.empty_like(x)
+    for ch in [int(c) for c in args.chunks.split(",")]:
+        t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=ch), args.steps, 3, torch.cuda.synchronize)
+        ms = t / args.steps * 1e3
+        print(json.dumps({"chunk": ch, "ms_per_apply": ms,
+                          "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
