@@ -28,9 +28,16 @@ constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 template <int P, int Q>
 struct RowCfg {
   static constexpr int BASE = 32 / cgcd(P, 32);
-  static constexpr int ROWS = BASE * ((128 / (BASE * P)) > 1 ? (128 / (BASE * P)) : 1);
+  static constexpr int ROWS0 = BASE * ((128 / (BASE * P)) > 1 ? (128 / (BASE * P)) : 1);
+  static constexpr int ROWS = ROWS0 > 64 ? 64 : ROWS0;
   static constexpr int T = ROWS * P;
-  static constexpr int MINB = (T <= 128) ? 4 : 3;
+  static constexpr int MINB = (T <= 160) ? 4 : 3;
+  static constexpr int MINB_INV = (T <= 128) ? 4 : 3;
+  static constexpr int N = P * Q;
+  static constexpr int XS = N + ((((P % 16) - (N % 16)) % 16 + 16) % 16);  // x row stride = P (mod 16)
+  // dynamic smem (float2): twiddles N | work rows ROWS*VS | [fwd only] staged x ROWS*XS
+  static constexpr size_t SMEM_FWD = sizeof(float2) * (N + ROWS * FftShape<P, Q>::VS + ROWS * XS);
+  static constexpr size_t SMEM_INV = sizeof(float2) * (N + ROWS * FftShape<P, Q>::VS);
 };
 
 template <int P, int Q>
@@ -40,8 +47,11 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          int ncoils, int ny, long long x_bstride, long long map_bstride) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
-  __shared__ float2 t1[N];
-  __shared__ __align__(16) float2 buf[ROWS * S::VS];
+  constexpr int XS = RowCfg<P, Q>::XS;
+  extern __shared__ __align__(16) float2 dsm[];
+  float2* t1 = dsm;
+  float2* buf = dsm + N;
+  float2* xs = buf + ROWS * S::VS;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
@@ -49,26 +59,31 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   const int row = row0 + lr;
   const bool valid = row < ny;
   const long long D = (long long)ny * N;
+  const int nvalid = min(ROWS, ny - row0) * N;
   init_tw_s1<P, Q>(t1, tid, T);
+  // stage u = x - anchor for the CTA's rows once; reused by every coil
+  {
+    const float2* xb = x + b * x_bstride + (long long)row0 * N;
+    const float2* ab = anchor ? anchor + b * x_bstride + (long long)row0 * N : nullptr;
+    for (int e = tid; e < ROWS * N; e += T) {
+      const int l3 = e / N, pos = e - l3 * N;
+      float2 v = make_float2(0.f, 0.f);
+      if (e < nvalid) {
+        v = __ldg(xb + e);
+        if (ab) v = csub(v, __ldg(ab + e));
+      }
+      xs[l3 * XS + pos] = v;
+    }
+  }
   __syncthreads();
-  const float2* xr = x + b * x_bstride + (long long)row * N + p;
-  const float2* ar = anchor ? anchor + b * x_bstride + (long long)row * N + p : nullptr;
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
-  const int nvalid = min(ROWS, ny - row0) * N;
+  const float2* xr = xs + lr * XS + p;
   for (int j = 0; j < ncoils; ++j) {
     float2 r[Q];
     const float2* mr = mb + j * D;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      float2 v = make_float2(0.f, 0.f);
-      if (valid) {
-        v = __ldg(xr + P * q);
-        if (ar) v = csub(v, __ldg(ar + P * q));
-        v = cmul(__ldg(mr + P * q), v);
-      }
-      r[q] = v;
-    }
+    for (int q = 0; q < Q; ++q) r[q] = valid ? cmul(__ldg(mr + P * q), xr[P * q]) : make_float2(0.f, 0.f);
     fft_s1_fwd<P, Q>(r, p, t1);
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
@@ -99,15 +114,16 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
 // Epilogue: out = s_acc * acc + s_u * u + s_d * d, coefficients per slice
 // (coef[b] = {s_acc, s_u, s_d, unused}); coef == nullptr -> out = acc.
 template <int P, int Q>
-__global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
+__global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB_INV)
 k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
          const float2* __restrict__ u, const float2* __restrict__ d) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
-  __shared__ float2 t2[N];
-  __shared__ __align__(16) float2 buf[ROWS * S::VS];
+  extern __shared__ __align__(16) float2 dsm[];
+  float2* t2 = dsm;
+  float2* buf = dsm + N;
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
@@ -329,8 +345,16 @@ __global__ void k_scatter(float2* __restrict__ ws, const int* __restrict__ spos,
 template <int P, int Q>
 int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, float2* ws,
                   int batch, int ncoils, int ny, long long xbs, long long mbs, cudaStream_t st) {
-  dim3 grid((ny + RowCfg<P, Q>::ROWS - 1) / RowCfg<P, Q>::ROWS, batch);
-  k_rowfwd<P, Q><<<grid, RowCfg<P, Q>::T, 0, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs);
+  using R = RowCfg<P, Q>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k_rowfwd<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)R::SMEM_FWD) != cudaSuccess)
+      return SR_ECUDA;
+    configured = true;
+  }
+  dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
+  k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -339,8 +363,16 @@ template <int P, int Q>
 int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, int ncoils,
                   int ny, long long xbs, long long mbs, const float4* coef, const float2* u,
                   const float2* d, cudaStream_t st) {
-  dim3 grid((ny + RowCfg<P, Q>::ROWS - 1) / RowCfg<P, Q>::ROWS, batch);
-  k_rowinv<P, Q><<<grid, RowCfg<P, Q>::T, 0, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d);
+  using R = RowCfg<P, Q>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k_rowinv<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)R::SMEM_INV) != cudaSuccess)
+      return SR_ECUDA;
+    configured = true;
+  }
+  dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
+  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
