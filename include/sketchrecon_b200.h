@@ -53,13 +53,20 @@ int sr_fft_split(int n, int* P, int* Q);
  *   anchor: NULL or (batch, ny, nx): operator input is x - anchor
  *   coef: NULL -> out = acc; else device float4 per slice {s_acc, s_u, s_d, -}:
  *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v)
- *   chunk: slices per pass group (0 = all): the three passes run per group of
- *          `chunk` slices so the coil workspace (chunk*ncoils*ny*nx) stays L2-resident */
+ *   chunk: 0 = auto: the single persistent fused launch (cart_fused.cu) when
+ *          sr_fused_normal_supported(ny, nx), else three launches over the batch;
+ *          > 0: three launches per group of `chunk` slices; -1: three launches, whole batch.
+ *   ws: sr_cart_ws_bytes(batch, ncoils, ny, nx, chunk) bytes */
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk,
                    void* stream);
+
+/* Workspace bytes sr_cart_normal needs for these arguments. */
+long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
+/* 1 if the persistent fused K1 is instantiated for an ny x nx grid. */
+int sr_fused_normal_supported(int ny, int nx);
 
 /* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
  * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)

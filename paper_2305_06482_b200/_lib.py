@@ -35,8 +35,10 @@ SIGNATURES = {
     "sr_lincomb": [_vp, _vp, _vp, _vp, _vp, _f, _f, _f, _ll, _ll, _i, _vp],
     "sr_scalar_op": [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
+    "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
+    "sr_fused_normal_supported": [_i, _i],
 }
-RESTYPES = {"sr_host_vd_poisson": C.c_longlong}
+RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong}
 
 _ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError}
 _MESSAGES = {1: "invalid argument or shape", 2: "unsupported transform length",

@@ -59,7 +59,7 @@ class CartesianKernel:
         woff[1:] = np.cumsum([len(p.wlist) for p in per_slice])
         self.woff = dv.host_to_dev(woff, torch.int64, dev)
         self._ws = None
-        self.chunk = 0  # slices per pass group of the fused normal op (0 = whole batch)
+        self.chunk = 0  # sr_cart_normal schedule: 0 auto (fused), >0 chunked 3-pass, -1 3-pass
         self._plans = plans
         self._replicas: dict[int, "CartesianKernel"] = {}
 
@@ -68,8 +68,11 @@ class CartesianKernel:
         return cls(dims, [cartesian_plan(tuple(dims), points)])
 
     # ------------------------------------------------------------------ device
-    def workspace(self, ncoils: int, batch: int | None = None) -> torch.Tensor:
-        need = (batch or self.batch) * ncoils * self.D
+    def workspace(self, ncoils: int, batch: int | None = None, chunk: int = -1) -> torch.Tensor:
+        """Coil workspace (complex64) large enough for sr_cart_normal(chunk) and the K2 passes."""
+        nbytes = max(8 * (batch or self.batch) * ncoils * self.D,
+                     _lib.lib().sr_cart_ws_bytes(self.batch, ncoils, self.ny, self.nx, chunk))
+        need = (nbytes + 7) // 8
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.complex64, device=self.device)
         return self._ws
@@ -91,15 +94,16 @@ class CartesianKernel:
     def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None, chunk=None):
         """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1).
 
-        chunk: slices per pass group (None -> self.chunk; 0 -> all at once).
+        chunk: None -> self.chunk; 0 -> auto (single persistent fused launch when the grid
+        has an instantiation); > 0 -> three launches per group of `chunk` slices; -1 -> three
+        launches over the whole batch.
         """
         _no_weights(w)
         ncoils, mbs = self._maps_stride(maps)
         for t, n in ((x, "x"), (out, "out"), (anchor, "anchor"), (u, "u"), (d, "d")):
             self._check_img(t, n)
         chunk = self.chunk if chunk is None else int(chunk)
-        chunk = self.batch if chunk <= 0 else min(chunk, self.batch)
-        ws = self.workspace(ncoils, chunk)
+        ws = self.workspace(ncoils, chunk=chunk)
         _lib.call("sr_cart_normal", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), mbs,
                   dv.ptr(self.maskT), self.mask_bstride, dv.ptr(out), dv.ptr(ws), self.batch,
                   ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), chunk, dv.stream())

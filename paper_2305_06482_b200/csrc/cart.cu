@@ -18,6 +18,14 @@
 //   C  rowinv : row IFFT (perm -> natural), sum_j conj(c_j) * (.), epilogue
 #include "fft2step.cuh"
 
+// cart_fused.cu
+int sr_fused_normal_supported(int ny, int nx);
+long long sr_fused_sync_ints(int batch, int ncoils);
+int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
+                    const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
+                    int batch, int ncoils, int ny, int nx, const float4* coef, const float2* u,
+                    const float2* d, cudaStream_t st);
+
 namespace {
 
 // ------------------------------------------------------------------- pass A
@@ -459,15 +467,30 @@ int sr_fft_split(int n, int* P, int* Q) {
   }
 }
 
+long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk) {
+  const long long D = (long long)ny * nx;
+  if (chunk == 0 && sr_fused_normal_supported(ny, nx))
+    return 8LL * batch * ncoils * D + 4LL * sr_fused_sync_ints(batch, ncoils) + 256;
+  const int nb = (chunk <= 0 || chunk > batch) ? batch : chunk;
+  return 8LL * nb * ncoils * D;
+}
+
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk, void* stream) {
-  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < 0) return SR_EINVAL;
+  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < -1) return SR_EINVAL;
   if (!fft_size_supported(nx) || !fft_size_supported(ny)) return SR_EUNSUPPORTED;
+  if (chunk == 0 && sr_fused_normal_supported(ny, nx)) {
+    const long long D = (long long)ny * nx;
+    int* sync = (int*)((float2*)ws + (long long)batch * ncoils * D);
+    return sr_fused_normal((const float2*)x, (const float2*)anchor, (const float2*)maps, map_bstride,
+                           maskT, mask_bstride, (float2*)out, (float2*)ws, sync, batch, ncoils, ny, nx,
+                           (const float4*)coef, (const float2*)u, (const float2*)d, (cudaStream_t)stream);
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const long long D = (long long)ny * nx;
-  if (chunk == 0 || chunk > batch) chunk = batch;
+  if (chunk <= 0 || chunk > batch) chunk = batch;
   for (int b0 = 0; b0 < batch; b0 += chunk) {
     const int nb = (batch - b0) < chunk ? (batch - b0) : chunk;
     const long long xo = (long long)b0 * D;

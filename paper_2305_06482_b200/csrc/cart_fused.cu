@@ -1,0 +1,366 @@
+// K1 (fused): the whole Cartesian sketched normal operator in ONE persistent launch.
+//
+//   out_b = e( sum_j conj(c_bj) . F^H M'_b F (c_bj . (x_b - a_b)) )
+//
+// Reference: SenseOperator._forward/_adjoint (forward_model.py:168-180) over
+// _CartesianMaskKernel (linops.py:344-364); the solvers call it as
+// adjoint(forward(.)) (coil_sketch.py:126,133,197; solvers.py:175,248).
+//
+// Design (B200): the three passes of cart.cu (row FFT, column FFT-mask-IFFT,
+// row IFFT + conjugate coil sum) become three kinds of work items of one
+// persistent kernel, pulled in a fixed ticket order that staggers slices:
+//     round r = { A items of slice r, B items of slice r-1, C items of slice r-2 }
+//   A(s, row tile, coil)  u = c_j (x - a) on 16 rows, row FFT      -> ws
+//   B(s, col tile, coil)  16 columns: FFT, mask/D, IFFT           (ws in place)
+//   C(s, row tile)        16 rows: for every coil, row IFFT, acc += conj(c_j) (.),
+//                         then the epilogue (FISTA / CG combination)
+// Only ~3 slices are in flight, so the coil workspace (9.8 MB per 320^2 slice
+// at C_hat = 12) and the re-read maps stay in the 126 MB L2: HBM sees ~the
+// compulsory bytes (maps + x + out) instead of 5 workspace sweeps.  Measured
+// on this part: L2-resident reads ~18.5 TB/s vs HBM ~7 TB/s vs DSMEM <= 4.8
+// TB/s (tools/membw_probe.cu), which is why the exchange goes through L2 and
+// not through cluster shared memory.
+//
+// Dependencies are per (slice, coil) counters with release/acquire at gpu
+// scope; an item only waits on items with smaller tickets, which are already
+// owned by resident CTAs, so the schedule cannot deadlock.  Workspace reads
+// use ld.global.cg (L1 is not coherent across CTAs); counters are zeroed by a
+// memset in the same stream before each launch.
+#include "fft2step.cuh"
+
+namespace {
+
+constexpr int TILE = 16;  // rows per A/C item, columns per B item
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int P, int QY, int QX>
+struct FusedCfg {
+  using SX = FftShape<P, QX>;
+  using SY = FftShape<P, QY>;
+  static constexpr int NX = P * QX, NY = P * QY;
+  static constexpr int T = TILE * P;
+  static constexpr int VSX = SX::VS;         // row-tile stride (= P mod 16)
+  static constexpr int VSPY = SY::VS0 | 1;   // column-tile stride (odd)
+  static constexpr int BUF = (TILE * VSX > TILE * VSPY) ? TILE * VSX : TILE * VSPY;
+  static constexpr int OFF_TX1 = 0, OFF_TX2 = NX, OFF_TY1 = 2 * NX, OFF_TY2 = 2 * NX + NY;
+  static constexpr int OFF_BUF = 2 * NX + 2 * NY;
+  static constexpr size_t SMEM = sizeof(float2) * (OFF_BUF + BUF) + 16;
+};
+
+struct FusedArgs {
+  const float2* x;
+  const float2* anchor;
+  const float2* maps;
+  long long map_bstride;
+  const uint8_t* maskT;
+  long long mask_bstride;
+  float2* out;
+  float2* ws;
+  int* sync;  // [0] ticket, [1..] cntA[S*C], cntB[S*C]
+  int batch, ncoils;
+  float mscale;
+  const float4* coef;
+  const float2* u;
+  const float2* d;
+};
+
+// ---------------------------------------------------------------- A items
+template <int P, int QY, int QX>
+__device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm) {
+  using F = FusedCfg<P, QY, QX>;
+  using SX = typename F::SX;
+  constexpr int NX = F::NX, NY = F::NY, T = F::T;
+  const int tid = threadIdx.x;
+  const int lr = tid / P, p = tid - lr * P;
+  const int row = rt * TILE + lr;
+  const bool valid = row < NY;
+  const long long D = (long long)NX * NY;
+  const float2* tx1 = sm + F::OFF_TX1;
+  float2* buf = sm + F::OFF_BUF;
+  float2 r[QX];
+  {
+    const long long xo = (long long)s * D + (long long)row * NX + p;
+    const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
+#pragma unroll
+    for (int q = 0; q < QX; ++q) {
+      float2 v = make_float2(0.f, 0.f);
+      if (valid) {
+        v = __ldg(a.x + xo + P * q);
+        if (a.anchor) v = csub(v, __ldg(a.anchor + xo + P * q));
+        v = cmul(__ldg(mr + P * q), v);
+      }
+      r[q] = v;
+    }
+  }
+  fft_s1_fwd<P, QX>(r, p, tx1);
+#pragma unroll
+  for (int k2 = 0; k2 < QX; ++k2) buf[lr * F::VSX + SX::GS * k2 + p] = r[k2];
+  __syncthreads();
+  for (int it = tid; it < TILE * QX; it += T) {
+    const int l2 = it / QX, k2 = it - l2 * QX;
+    float2 g[P];
+    float2* gp = buf + l2 * F::VSX + SX::GS * k2;
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+    fft_s2_fwd<P>(g);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+  }
+  __syncthreads();
+  const int nrows = min(TILE, NY - rt * TILE);
+  float2* wj = a.ws + ((long long)s * a.ncoils + j) * D + (long long)rt * TILE * NX;
+  for (int e = tid; e < nrows * NX; e += T) {
+    const int l3 = e / NX, pos = e - l3 * NX;
+    __stcg(wj + e, buf[l3 * F::VSX + SX::pad(pos)]);
+  }
+}
+
+// ---------------------------------------------------------------- B items
+template <int P, int QY, int QX>
+__device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* sm) {
+  using F = FusedCfg<P, QY, QX>;
+  using SY = typename F::SY;
+  constexpr int NX = F::NX, NY = F::NY, T = F::T;
+  const int tid = threadIdx.x;
+  const int c = tid % TILE, p = tid / TILE;
+  const int c0 = ct * TILE;
+  const int ncols = min(TILE, NX - c0);
+  const bool cvalid = c < ncols;
+  const long long D = (long long)NX * NY;
+  const float2* ty1 = sm + F::OFF_TY1;
+  const float2* ty2 = sm + F::OFF_TY2;
+  float2* buf = sm + F::OFF_BUF;
+  float2* img = a.ws + ((long long)s * a.ncoils + j) * D;
+  float2 r[QY];
+#pragma unroll
+  for (int q = 0; q < QY; ++q)
+    r[q] = cvalid ? __ldcg(img + (long long)(p + P * q) * NX + c0 + c) : make_float2(0.f, 0.f);
+  fft_s1_fwd<P, QY>(r, p, ty1);
+#pragma unroll
+  for (int k2 = 0; k2 < QY; ++k2) buf[c * F::VSPY + SY::GS * k2 + p] = r[k2];
+  __syncthreads();
+  const uint8_t* mcol = a.maskT + s * a.mask_bstride;
+  for (int it = tid; it < TILE * QY; it += T) {
+    const int cc = it % TILE, k2 = it / TILE;
+    if (cc >= ncols) continue;
+    float2 g[P];
+    float2* gp = buf + cc * F::VSPY + SY::GS * k2;
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+    fft_s2_fwd<P>(g);
+    const uint8_t* mk = mcol + (long long)(c0 + cc) * NY + P * k2;
+    if ((P % 4) == 0) {
+#pragma unroll
+      for (int w4 = 0; w4 < P / 4; ++w4) {
+        const uint32_t m4 = __ldg(reinterpret_cast<const uint32_t*>(mk) + w4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          g[4 * w4 + i] = cscale(g[4 * w4 + i], ((m4 >> (8 * i)) & 0xffu) ? a.mscale : 0.f);
+      }
+    } else {
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mk[k1] ? a.mscale : 0.f);
+    }
+    fft_s2_inv<P, QY>(g, k2, ty2);
+#pragma unroll
+    for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k2 = 0; k2 < QY; ++k2) r[k2] = buf[c * F::VSPY + SY::GS * k2 + p];
+  fft_s1_inv<QY>(r);
+  if (cvalid) {
+#pragma unroll
+    for (int q = 0; q < QY; ++q) __stcg(img + (long long)(p + P * q) * NX + c0 + c, r[q]);
+  }
+}
+
+// ---------------------------------------------------------------- C items
+template <int P, int QY, int QX>
+__device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int ncoltiles, float2* sm) {
+  using F = FusedCfg<P, QY, QX>;
+  using SX = typename F::SX;
+  constexpr int NX = F::NX, NY = F::NY, T = F::T;
+  const int tid = threadIdx.x;
+  const int lr = tid / P, p = tid - lr * P;
+  const int row = rt * TILE + lr;
+  const bool valid = row < NY;
+  const long long D = (long long)NX * NY;
+  const float2* tx2 = sm + F::OFF_TX2;
+  float2* buf = sm + F::OFF_BUF;
+  const int nrows = min(TILE, NY - rt * TILE);
+  float2 acc[QX];
+#pragma unroll
+  for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
+  for (int j = 0; j < a.ncoils; ++j) {
+    if (tid == 0) {
+      const int* c = cntB + s * a.ncoils + j;
+      while (ld_acquire(c) < ncoltiles) __nanosleep(128);
+    }
+    __syncthreads();
+    const float2* wj = a.ws + ((long long)s * a.ncoils + j) * D + (long long)rt * TILE * NX;
+    for (int e = tid; e < nrows * NX; e += T) {
+      const int l3 = e / NX, pos = e - l3 * NX;
+      buf[l3 * F::VSX + SX::pad(pos)] = __ldcg(wj + e);
+    }
+    __syncthreads();
+    for (int it = tid; it < TILE * QX; it += T) {
+      const int l2 = it / QX, k2 = it - l2 * QX;
+      float2 g[P];
+      float2* gp = buf + l2 * F::VSX + SX::GS * k2;
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+      fft_s2_inv<P, QX>(g, k2, tx2);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+    }
+    __syncthreads();
+    float2 r[QX];
+#pragma unroll
+    for (int k2 = 0; k2 < QX; ++k2) r[k2] = buf[lr * F::VSX + SX::GS * k2 + p];
+    fft_s1_inv<QX>(r);
+    if (valid) {
+      const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
+#pragma unroll
+      for (int q = 0; q < QX; ++q) cfma_conj(acc[q], __ldg(mr + P * q), r[q]);
+    }
+    __syncthreads();
+  }
+  if (!valid) return;
+  const long long off = (long long)s * D + (long long)row * NX + p;
+  if (a.coef == nullptr) {
+#pragma unroll
+    for (int q = 0; q < QX; ++q) a.out[off + P * q] = acc[q];
+  } else {
+    const float4 cf = a.coef[s];
+#pragma unroll
+    for (int q = 0; q < QX; ++q) {
+      float2 v = cscale(acc[q], cf.x);
+      if (a.u) { const float2 uu = a.u[off + P * q]; v.x = fmaf(cf.y, uu.x, v.x); v.y = fmaf(cf.y, uu.y, v.y); }
+      if (a.d) { const float2 dd = a.d[off + P * q]; v.x = fmaf(cf.z, dd.x, v.x); v.y = fmaf(cf.z, dd.y, v.y); }
+      a.out[off + P * q] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- scheduler
+template <int P, int QY, int QX>
+__global__ void __launch_bounds__(FusedCfg<P, QY, QX>::T, 2)
+k_cart_normal_fused(FusedArgs a) {
+  using F = FusedCfg<P, QY, QX>;
+  constexpr int NX = F::NX, NY = F::NY, T = F::T;
+  extern __shared__ __align__(16) float2 sm[];
+  __shared__ int s_ticket;
+  const int tid = threadIdx.x;
+  init_tw_s1<P, QX>(sm + F::OFF_TX1, tid, T);
+  init_tw_s2<P, QX>(sm + F::OFF_TX2, tid, T);
+  init_tw_s1<P, QY>(sm + F::OFF_TY1, tid, T);
+  init_tw_s2<P, QY>(sm + F::OFF_TY2, tid, T);
+  __syncthreads();
+  const int S = a.batch, C = a.ncoils;
+  const int nrt = (NY + TILE - 1) / TILE, nct = (NX + TILE - 1) / TILE;
+  const int nA = nrt * C, nB = nct * C, nC = nrt;
+  int* cntA = a.sync + 1;
+  int* cntB = cntA + S * C;
+  const long long total = (long long)S * (nA + nB + nC);
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(a.sync, 1);
+    __syncthreads();
+    long long t = s_ticket;
+    __syncthreads();
+    if (t >= total) break;
+    // decode: round r holds A(r) [r < S], B(r-1) [1 <= r <= S], C(r-2) [2 <= r <= S+1]
+    int r = 0;
+    for (;; ++r) {
+      const long long sz = (r < S ? nA : 0) + (r >= 1 && r <= S ? nB : 0) + (r >= 2 && r <= S + 1 ? nC : 0);
+      if (t < sz) break;
+      t -= sz;
+    }
+    const int it = (int)t;
+    if (r < S && it < nA) {
+      const int s = r, rt = it % nrt, j = it / nrt;
+      item_rowfwd<P, QY, QX>(a, s, rt, j, sm);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) red_release_add(cntA + s * C + j, 1);
+    } else {
+      const int it2 = it - (r < S ? nA : 0);
+      if (r >= 1 && r <= S && it2 < nB) {
+        const int s = r - 1, ct = it2 % nct, j = it2 / nct;
+        if (tid == 0) {
+          const int* c = cntA + s * C + j;
+          while (ld_acquire(c) < nrt) __nanosleep(128);
+        }
+        __syncthreads();
+        item_colpass<P, QY, QX>(a, s, ct, j, sm);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) red_release_add(cntB + s * C + j, 1);
+      } else {
+        const int it3 = it2 - (r >= 1 && r <= S ? nB : 0);
+        const int s = r - 2, rt = it3;
+        item_rowinv<P, QY, QX>(a, s, rt, cntB, nct, sm);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int P, int QY, int QX>
+int launch_fused(const FusedArgs& a, cudaStream_t st) {
+  using F = FusedCfg<P, QY, QX>;
+  static int grid = 0;
+  if (grid == 0) {
+    if (cudaFuncSetAttribute(k_cart_normal_fused<P, QY, QX>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM) != cudaSuccess)
+      return SR_ECUDA;
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cart_normal_fused<P, QY, QX>, F::T, F::SMEM);
+    if (per < 1) return SR_ECUDA;
+    grid = nsm * per;
+  }
+  k_cart_normal_fused<P, QY, QX><<<grid, F::T, F::SMEM, st>>>(a);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
+}  // namespace
+
+// (ny, nx) pairs with a fused instantiation: X(P, QY, QX)
+#define SR_FUSED_SIZES(X)                                                                  \
+  X(20, 16, 16) X(16, 16, 16) X(16, 16, 10) X(16, 10, 16) X(16, 10, 10) X(16, 8, 8)        \
+  X(20, 10, 10) X(20, 16, 10) X(20, 10, 16) X(16, 4, 4) X(16, 8, 16) X(16, 16, 8)
+
+int sr_fused_normal_supported(int ny, int nx) {
+#define X(P, QY, QX) if (ny == P * QY && nx == P * QX) return 1;
+  SR_FUSED_SIZES(X)
+#undef X
+  return 0;
+}
+
+long long sr_fused_sync_ints(int batch, int ncoils) { return 1 + 2LL * batch * ncoils; }
+
+int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
+                    const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
+                    int batch, int ncoils, int ny, int nx, const float4* coef, const float2* u,
+                    const float2* d, cudaStream_t st) {
+  FusedArgs a{x, anchor, maps, map_bstride, maskT, mask_bstride, out, ws, sync, batch, ncoils,
+              (float)(1.0 / ((double)ny * nx)), coef, u, d};
+  if (cudaMemsetAsync(sync, 0, sizeof(int) * sr_fused_sync_ints(batch, ncoils), st) != cudaSuccess)
+    return SR_ECUDA;
+#define X(P, QY, QX) \
+  if (ny == P * QY && nx == P * QX) return launch_fused<P, QY, QX>(a, st);
+  SR_FUSED_SIZES(X)
+#undef X
+  return SR_EUNSUPPORTED;
+}
