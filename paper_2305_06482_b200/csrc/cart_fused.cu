@@ -30,7 +30,9 @@
 
 namespace {
 
-constexpr int TILE = 16;  // rows per A/C item, columns per B item
+constexpr int TILE = 16;   // rows per A/C item, columns per B item
+constexpr int WSLOTS = 4;  // workspace ring: slice s lives in slot s % WSLOTS (stays in L2,
+                           // and its dirty lines are overwritten before they are evicted)
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -63,8 +65,8 @@ struct FusedArgs {
   const uint8_t* maskT;
   long long mask_bstride;
   float2* out;
-  float2* ws;
-  int* sync;  // [0] ticket, [1..] cntA[S*C], cntB[S*C]
+  float2* ws;     // ring of WSLOTS slice slots of (C, ny, nx)
+  int* sync;      // [0] ticket, [1..] cntA[S*C], cntB[S*C], cntC[S]
   int batch, ncoils;
   float mscale;
   const float4* coef;
@@ -116,7 +118,7 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm
   }
   __syncthreads();
   const int nrows = min(TILE, NY - rt * TILE);
-  float2* wj = a.ws + ((long long)s * a.ncoils + j) * D + (long long)rt * TILE * NX;
+  float2* wj = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D + (long long)rt * TILE * NX;
   for (int e = tid; e < nrows * NX; e += T) {
     const int l3 = e / NX, pos = e - l3 * NX;
     __stcg(wj + e, buf[l3 * F::VSX + SX::pad(pos)]);
@@ -138,7 +140,7 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   const float2* ty1 = sm + F::OFF_TY1;
   const float2* ty2 = sm + F::OFF_TY2;
   float2* buf = sm + F::OFF_BUF;
-  float2* img = a.ws + ((long long)s * a.ncoils + j) * D;
+  float2* img = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D;
   float2 r[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q)
@@ -206,7 +208,7 @@ __device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int nc
       while (ld_acquire(c) < ncoltiles) __nanosleep(128);
     }
     __syncthreads();
-    const float2* wj = a.ws + ((long long)s * a.ncoils + j) * D + (long long)rt * TILE * NX;
+    const float2* wj = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D + (long long)rt * TILE * NX;
     for (int e = tid; e < nrows * NX; e += T) {
       const int l3 = e / NX, pos = e - l3 * NX;
       buf[l3 * F::VSX + SX::pad(pos)] = __ldcg(wj + e);
@@ -270,6 +272,7 @@ k_cart_normal_fused(FusedArgs a) {
   const int nA = nrt * C, nB = nct * C, nC = nrt;
   int* cntA = a.sync + 1;
   int* cntB = cntA + S * C;
+  int* cntC = cntB + S * C;
   const long long total = (long long)S * (nA + nB + nC);
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(a.sync, 1);
@@ -287,8 +290,14 @@ k_cart_normal_fused(FusedArgs a) {
     const int it = (int)t;
     if (r < S && it < nA) {
       const int s = r, rt = it % nrt, j = it / nrt;
+      if (s >= WSLOTS) {  // slot reuse: every C item of slice s - WSLOTS has read it
+        if (tid == 0) {
+          const int* c = cntC + (s - WSLOTS);
+          while (ld_acquire(c) < nrt) __nanosleep(128);
+        }
+        __syncthreads();
+      }
       item_rowfwd<P, QY, QX>(a, s, rt, j, sm);
-      __threadfence();
       __syncthreads();
       if (tid == 0) red_release_add(cntA + s * C + j, 1);
     } else {
@@ -301,13 +310,14 @@ k_cart_normal_fused(FusedArgs a) {
         }
         __syncthreads();
         item_colpass<P, QY, QX>(a, s, ct, j, sm);
-        __threadfence();
         __syncthreads();
         if (tid == 0) red_release_add(cntB + s * C + j, 1);
       } else {
         const int it3 = it2 - (r >= 1 && r <= S ? nB : 0);
         const int s = r - 2, rt = it3;
         item_rowinv<P, QY, QX>(a, s, rt, cntB, nct, sm);
+        __syncthreads();
+        if (tid == 0) red_release_add(cntC + s, 1);
       }
     }
     __syncthreads();
@@ -348,7 +358,8 @@ int sr_fused_normal_supported(int ny, int nx) {
   return 0;
 }
 
-long long sr_fused_sync_ints(int batch, int ncoils) { return 1 + 2LL * batch * ncoils; }
+long long sr_fused_sync_ints(int batch, int ncoils) { return 1 + 2LL * batch * ncoils + batch; }
+long long sr_fused_ws_slices(int batch) { return batch < WSLOTS ? batch : WSLOTS; }
 
 int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
                     const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
