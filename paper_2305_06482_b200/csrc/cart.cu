@@ -20,8 +20,8 @@
 
 // cart_fused.cu
 int sr_fused_normal_supported(int ny, int nx);
-long long sr_fused_sync_ints(int batch, int ncoils);
-long long sr_fused_ws_slices(int batch);
+long long sr_fused_sync_ints(int batch, int ncoils, int ny);
+long long sr_fused_ws_elems(int batch, int ncoils, long long D);
 int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
                     const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
                     int batch, int ncoils, int ny, int nx, const float4* coef, const float2* u,
@@ -471,7 +471,7 @@ int sr_fft_split(int n, int* P, int* Q) {
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk) {
   const long long D = (long long)ny * nx;
   if (chunk == 0 && sr_fused_normal_supported(ny, nx))
-    return 8LL * sr_fused_ws_slices(batch) * ncoils * D + 4LL * sr_fused_sync_ints(batch, ncoils) + 256;
+    return 8LL * sr_fused_ws_elems(batch, ncoils, D) + 4LL * sr_fused_sync_ints(batch, ncoils, ny) + 256;
   const int nb = (chunk <= 0 || chunk > batch) ? batch : chunk;
   return 8LL * nb * ncoils * D;
 }
@@ -484,7 +484,7 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
   if (!fft_size_supported(nx) || !fft_size_supported(ny)) return SR_EUNSUPPORTED;
   if (chunk == 0 && sr_fused_normal_supported(ny, nx)) {
     const long long D = (long long)ny * nx;
-    int* sync = (int*)((float2*)ws + sr_fused_ws_slices(batch) * ncoils * D);
+    int* sync = (int*)((float2*)ws + sr_fused_ws_elems(batch, ncoils, D));
     return sr_fused_normal((const float2*)x, (const float2*)anchor, (const float2*)maps, map_bstride,
                            maskT, mask_bstride, (float2*)out, (float2*)ws, sync, batch, ncoils, ny, nx,
                            (const float4*)coef, (const float2*)u, (const float2*)d, (cudaStream_t)stream);

@@ -186,8 +186,19 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
 }
 
 // ---------------------------------------------------------------- C items
+__device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// C(s, rt, g): coils [g*CG, g*CG + CG) of 16 rows; partial sums go to the
+// partial ring, the last group to finish a row tile sums the G partials in a
+// fixed order (deterministic) and writes the epilogue.  Returns true when this
+// item finalised the row tile.
 template <int P, int QY, int QX>
-__device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int ncoltiles, float2* sm) {
+__device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int CG, int* cntB,
+                            int* cntT, int ncoltiles, float2* sm, int* s_flag) {
   using F = FusedCfg<P, QY, QX>;
   using SX = typename F::SX;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
@@ -199,16 +210,18 @@ __device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int nc
   const float2* tx2 = sm + F::OFF_TX2;
   float2* buf = sm + F::OFF_BUF;
   const int nrows = min(TILE, NY - rt * TILE);
+  const int slot = s % WSLOTS;
   float2 acc[QX];
 #pragma unroll
   for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
-  for (int j = 0; j < a.ncoils; ++j) {
+  const int j0 = g * CG, j1 = min(a.ncoils, j0 + CG);
+  for (int j = j0; j < j1; ++j) {
     if (tid == 0) {
       const int* c = cntB + s * a.ncoils + j;
-      while (ld_acquire(c) < ncoltiles) __nanosleep(128);
+      while (ld_acquire(c) < ncoltiles) __nanosleep(64);
     }
     __syncthreads();
-    const float2* wj = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D + (long long)rt * TILE * NX;
+    const float2* wj = a.ws + ((long long)slot * a.ncoils + j) * D + (long long)rt * TILE * NX;
     for (int e = tid; e < nrows * NX; e += T) {
       const int l3 = e / NX, pos = e - l3 * NX;
       buf[l3 * F::VSX + SX::pad(pos)] = __ldcg(wj + e);
@@ -216,13 +229,13 @@ __device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int nc
     __syncthreads();
     for (int it = tid; it < TILE * QX; it += T) {
       const int l2 = it / QX, k2 = it - l2 * QX;
-      float2 g[P];
+      float2 gg[P];
       float2* gp = buf + l2 * F::VSX + SX::GS * k2;
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-      fft_s2_inv<P, QX>(g, k2, tx2);
+      for (int k1 = 0; k1 < P; ++k1) gg[k1] = gp[k1];
+      fft_s2_inv<P, QX>(gg, k2, tx2);
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      for (int k1 = 0; k1 < P; ++k1) gp[k1] = gg[k1];
     }
     __syncthreads();
     float2 r[QX];
@@ -236,8 +249,29 @@ __device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int nc
     }
     __syncthreads();
   }
-  if (!valid) return;
-  const long long off = (long long)s * D + (long long)row * NX + p;
+  const long long roff = (long long)row * NX + p;
+  if (G > 1) {
+    float2* part = a.ws + (long long)WSLOTS * a.ncoils * D + ((long long)slot * G + g) * D;
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < QX; ++q) __stcg(part + roff + P * q, acc[q]);
+    }
+    __syncthreads();
+    if (tid == 0) *s_flag = (atom_add_acqrel(cntT + s * ((NY + TILE - 1) / TILE) + rt, 1) == G - 1);
+    __syncthreads();
+    if (!*s_flag) return false;
+    const float2* pb = a.ws + (long long)WSLOTS * a.ncoils * D + (long long)slot * G * D;
+#pragma unroll
+    for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
+    if (valid) {
+      for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+        for (int q = 0; q < QX; ++q) acc[q] = cadd(acc[q], __ldcg(pb + (long long)gg * D + roff + P * q));
+      }
+    }
+  }
+  if (!valid) return true;
+  const long long off = (long long)s * D + roff;
   if (a.coef == nullptr) {
 #pragma unroll
     for (int q = 0; q < QX; ++q) a.out[off + P * q] = acc[q];
@@ -251,16 +285,19 @@ __device__ void item_rowinv(const FusedArgs& a, int s, int rt, int* cntB, int nc
       a.out[off + P * q] = v;
     }
   }
+  return true;
 }
 
 // ---------------------------------------------------------------- scheduler
+constexpr int COILS_PER_C = 3;  // coils per C item (partial coil sums, G = ceil(C / 3) groups)
+
 template <int P, int QY, int QX>
 __global__ void __launch_bounds__(FusedCfg<P, QY, QX>::T, 2)
 k_cart_normal_fused(FusedArgs a) {
   using F = FusedCfg<P, QY, QX>;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
   extern __shared__ __align__(16) float2 sm[];
-  __shared__ int s_ticket;
+  __shared__ int s_ticket, s_flag;
   const int tid = threadIdx.x;
   init_tw_s1<P, QX>(sm + F::OFF_TX1, tid, T);
   init_tw_s2<P, QX>(sm + F::OFF_TX2, tid, T);
@@ -269,10 +306,12 @@ k_cart_normal_fused(FusedArgs a) {
   __syncthreads();
   const int S = a.batch, C = a.ncoils;
   const int nrt = (NY + TILE - 1) / TILE, nct = (NX + TILE - 1) / TILE;
-  const int nA = nrt * C, nB = nct * C, nC = nrt;
+  const int G = (C + COILS_PER_C - 1) / COILS_PER_C;
+  const int nA = nrt * C, nB = nct * C, nC = nrt * G;
   int* cntA = a.sync + 1;
   int* cntB = cntA + S * C;
-  int* cntC = cntB + S * C;
+  int* cntC = cntB + S * C;     // finalised row tiles per slice
+  int* cntT = cntC + S;         // finished coil groups per (slice, row tile)
   const long long total = (long long)S * (nA + nB + nC);
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(a.sync, 1);
@@ -280,7 +319,7 @@ k_cart_normal_fused(FusedArgs a) {
     long long t = s_ticket;
     __syncthreads();
     if (t >= total) break;
-    // decode: round r holds A(r) [r < S], B(r-1) [1 <= r <= S], C(r-2) [2 <= r <= S+1]
+    // round r holds A(r) [r < S], B(r-1) [1 <= r <= S], C(r-2) [2 <= r <= S+1]
     int r = 0;
     for (;; ++r) {
       const long long sz = (r < S ? nA : 0) + (r >= 1 && r <= S ? nB : 0) + (r >= 2 && r <= S + 1 ? nC : 0);
@@ -290,10 +329,10 @@ k_cart_normal_fused(FusedArgs a) {
     const int it = (int)t;
     if (r < S && it < nA) {
       const int s = r, rt = it % nrt, j = it / nrt;
-      if (s >= WSLOTS) {  // slot reuse: every C item of slice s - WSLOTS has read it
+      if (s >= WSLOTS) {  // slot reuse: every row tile of slice s - WSLOTS is final
         if (tid == 0) {
           const int* c = cntC + (s - WSLOTS);
-          while (ld_acquire(c) < nrt) __nanosleep(128);
+          while (ld_acquire(c) < nrt) __nanosleep(64);
         }
         __syncthreads();
       }
@@ -306,7 +345,7 @@ k_cart_normal_fused(FusedArgs a) {
         const int s = r - 1, ct = it2 % nct, j = it2 / nct;
         if (tid == 0) {
           const int* c = cntA + s * C + j;
-          while (ld_acquire(c) < nrt) __nanosleep(128);
+          while (ld_acquire(c) < nrt) __nanosleep(64);
         }
         __syncthreads();
         item_colpass<P, QY, QX>(a, s, ct, j, sm);
@@ -314,10 +353,10 @@ k_cart_normal_fused(FusedArgs a) {
         if (tid == 0) red_release_add(cntB + s * C + j, 1);
       } else {
         const int it3 = it2 - (r >= 1 && r <= S ? nB : 0);
-        const int s = r - 2, rt = it3;
-        item_rowinv<P, QY, QX>(a, s, rt, cntB, nct, sm);
+        const int s = r - 2, rt = it3 % nrt, g = it3 / nrt;
+        const bool fin = item_rowinv<P, QY, QX>(a, s, rt, g, G, COILS_PER_C, cntB, cntT, nct, sm, &s_flag);
         __syncthreads();
-        if (tid == 0) red_release_add(cntC + s, 1);
+        if (fin && tid == 0) red_release_add(cntC + s, 1);
       }
     }
     __syncthreads();
@@ -358,8 +397,14 @@ int sr_fused_normal_supported(int ny, int nx) {
   return 0;
 }
 
-long long sr_fused_sync_ints(int batch, int ncoils) { return 1 + 2LL * batch * ncoils + batch; }
-long long sr_fused_ws_slices(int batch) { return batch < WSLOTS ? batch : WSLOTS; }
+long long sr_fused_sync_ints(int batch, int ncoils, int ny) {
+  return 1 + 2LL * batch * ncoils + batch + (long long)batch * ((ny + TILE - 1) / TILE);
+}
+// complex64 elements of workspace: coil ring + partial-sum ring
+long long sr_fused_ws_elems(int batch, int ncoils, long long D) {
+  const long long G = (ncoils + COILS_PER_C - 1) / COILS_PER_C;
+  return (long long)WSLOTS * ncoils * D + (G > 1 ? (long long)WSLOTS * G * D : 0);
+}
 
 int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
                     const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
@@ -367,7 +412,7 @@ int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, l
                     const float2* d, cudaStream_t st) {
   FusedArgs a{x, anchor, maps, map_bstride, maskT, mask_bstride, out, ws, sync, batch, ncoils,
               (float)(1.0 / ((double)ny * nx)), coef, u, d};
-  if (cudaMemsetAsync(sync, 0, sizeof(int) * sr_fused_sync_ints(batch, ncoils), st) != cudaSuccess)
+  if (cudaMemsetAsync(sync, 0, sizeof(int) * sr_fused_sync_ints(batch, ncoils, ny), st) != cudaSuccess)
     return SR_ECUDA;
 #define X(P, QY, QX) \
   if (ny == P * QY && nx == P * QX) return launch_fused<P, QY, QX>(a, st);
