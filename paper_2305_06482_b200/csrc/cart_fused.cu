@@ -43,6 +43,34 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// L2 residency hints: the workspace ring is kept (evict_last); maps are read
+// twice (A, then C) and dropped after the second read (evict_first).
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float2 ld_ws(const float2* ptr, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_ws(float2* ptr, float2 v, uint64_t pol) {
+  asm volatile("st.global.cg.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;"
+               :: "l"(ptr), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float2 ld_ro_hint(const float2* ptr, uint64_t pol) {
+  float2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(ptr), "l"(pol));
+  return v;
+}
+
 template <int P, int QY, int QX>
 struct FusedCfg {
   using SX = FftShape<P, QX>;
@@ -121,7 +149,7 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm
   float2* wj = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D + (long long)rt * TILE * NX;
   for (int e = tid; e < nrows * NX; e += T) {
     const int l3 = e / NX, pos = e - l3 * NX;
-    __stcg(wj + e, buf[l3 * F::VSX + SX::pad(pos)]);
+    st_ws(wj + e, buf[l3 * F::VSX + SX::pad(pos)], pol_evict_last());
   }
 }
 
@@ -144,7 +172,7 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   float2 r[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q)
-    r[q] = cvalid ? __ldcg(img + (long long)(p + P * q) * NX + c0 + c) : make_float2(0.f, 0.f);
+    r[q] = cvalid ? ld_ws(img + (long long)(p + P * q) * NX + c0 + c, pol_evict_last()) : make_float2(0.f, 0.f);
   fft_s1_fwd<P, QY>(r, p, ty1);
 #pragma unroll
   for (int k2 = 0; k2 < QY; ++k2) buf[c * F::VSPY + SY::GS * k2 + p] = r[k2];
@@ -181,7 +209,7 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   fft_s1_inv<QY>(r);
   if (cvalid) {
 #pragma unroll
-    for (int q = 0; q < QY; ++q) __stcg(img + (long long)(p + P * q) * NX + c0 + c, r[q]);
+    for (int q = 0; q < QY; ++q) st_ws(img + (long long)(p + P * q) * NX + c0 + c, r[q], pol_evict_last());
   }
 }
 
@@ -224,7 +252,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
     const float2* wj = a.ws + ((long long)slot * a.ncoils + j) * D + (long long)rt * TILE * NX;
     for (int e = tid; e < nrows * NX; e += T) {
       const int l3 = e / NX, pos = e - l3 * NX;
-      buf[l3 * F::VSX + SX::pad(pos)] = __ldcg(wj + e);
+      buf[l3 * F::VSX + SX::pad(pos)] = ld_ws(wj + e, pol_evict_first());
     }
     __syncthreads();
     for (int it = tid; it < TILE * QX; it += T) {
@@ -245,7 +273,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
     if (valid) {
       const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
 #pragma unroll
-      for (int q = 0; q < QX; ++q) cfma_conj(acc[q], __ldg(mr + P * q), r[q]);
+      for (int q = 0; q < QX; ++q) cfma_conj(acc[q], ld_ro_hint(mr + P * q, pol_evict_first()), r[q]);
     }
     __syncthreads();
   }
@@ -254,7 +282,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
     float2* part = a.ws + (long long)WSLOTS * a.ncoils * D + ((long long)slot * G + g) * D;
     if (valid) {
 #pragma unroll
-      for (int q = 0; q < QX; ++q) __stcg(part + roff + P * q, acc[q]);
+      for (int q = 0; q < QX; ++q) st_ws(part + roff + P * q, acc[q], pol_evict_last());
     }
     __syncthreads();
     if (tid == 0) *s_flag = (atom_add_acqrel(cntT + s * ((NY + TILE - 1) / TILE) + rt, 1) == G - 1);
@@ -266,7 +294,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
     if (valid) {
       for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-        for (int q = 0; q < QX; ++q) acc[q] = cadd(acc[q], __ldcg(pb + (long long)gg * D + roff + P * q));
+        for (int q = 0; q < QX; ++q) acc[q] = cadd(acc[q], ld_ws(pb + (long long)gg * D + roff + P * q, pol_evict_first()));
       }
     }
   }
@@ -321,10 +349,30 @@ k_cart_normal_fused(FusedArgs a) {
     if (t >= total) break;
     // round r holds A(r) [r < S], B(r-1) [1 <= r <= S], C(r-2) [2 <= r <= S+1]
     int r = 0;
-    for (;; ++r) {
-      const long long sz = (r < S ? nA : 0) + (r >= 1 && r <= S ? nB : 0) + (r >= 2 && r <= S + 1 ? nC : 0);
-      if (t < sz) break;
-      t -= sz;
+    if (S >= 3) {  // closed form: rounds 2..S-1 are full
+      const long long full = nA + nB + nC;
+      if (t < nA) {
+        r = 0;
+      } else if ((t -= nA) < nA + nB) {
+        r = 1;
+      } else {
+        t -= nA + nB;
+        const long long k = t / full;
+        if (k < S - 2) {
+          r = 2 + (int)k;
+          t -= k * full;
+        } else {
+          t -= (long long)(S - 2) * full;
+          if (t < nB + nC) r = S;
+          else { r = S + 1; t -= nB + nC; }
+        }
+      }
+    } else {
+      for (;; ++r) {
+        const long long sz = (r < S ? nA : 0) + (r >= 1 && r <= S ? nB : 0) + (r >= 2 && r <= S + 1 ? nC : 0);
+        if (t < sz) break;
+        t -= sz;
+      }
     }
     const int it = (int)t;
     if (r < S && it < nA) {
