@@ -67,6 +67,9 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
 /* 1 if the persistent fused K1 is instantiated for an ny x nx grid. */
 int sr_fused_normal_supported(int ny, int nx);
+/* Schedule of the fused K1 (process-wide): round r runs A(r), B(r - lagB), C(r - lagC);
+ * `slots` slice slots of workspace ring (lagC < slots <= 8); tile = 8 or 16 rows/columns per item. */
+int sr_fused_config(int lagB, int lagC, int slots, int tile);
 
 /* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
  * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)

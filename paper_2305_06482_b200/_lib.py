@@ -37,6 +37,7 @@ SIGNATURES = {
     "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
     "sr_fused_normal_supported": [_i, _i],
+    "sr_fused_config": [_i, _i, _i, _i],
 }
 RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong}
 

@@ -30,9 +30,9 @@
 
 namespace {
 
-constexpr int TILE = 16;   // rows per A/C item, columns per B item
-constexpr int WSLOTS = 4;  // workspace ring: slice s lives in slot s % WSLOTS (stays in L2,
-                           // and its dirty lines are overwritten before they are evicted)
+constexpr int MAX_SLOTS = 8;  // workspace ring capacity (runtime `slots` <= MAX_SLOTS): slice s
+                              // lives in slot s % slots, stays in L2, and its dirty lines are
+                              // overwritten before they would be evicted
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -71,7 +71,7 @@ __device__ __forceinline__ float2 ld_ro_hint(const float2* ptr, uint64_t pol) {
   return v;
 }
 
-template <int P, int QY, int QX>
+template <int P, int QY, int QX, int TILE>
 struct FusedCfg {
   using SX = FftShape<P, QX>;
   using SY = FftShape<P, QY>;
@@ -82,7 +82,7 @@ struct FusedCfg {
   static constexpr int BUF = (TILE * VSX > TILE * VSPY) ? TILE * VSX : TILE * VSPY;
   static constexpr int OFF_TX1 = 0, OFF_TX2 = NX, OFF_TY1 = 2 * NX, OFF_TY2 = 2 * NX + NY;
   static constexpr int OFF_BUF = 2 * NX + 2 * NY;
-  static constexpr size_t SMEM = sizeof(float2) * (OFF_BUF + BUF) + 16;
+  static constexpr size_t SMEM = sizeof(float2) * (OFF_BUF + BUF) + 16;  // + round table (ints)
 };
 
 struct FusedArgs {
@@ -93,9 +93,10 @@ struct FusedArgs {
   const uint8_t* maskT;
   long long mask_bstride;
   float2* out;
-  float2* ws;     // ring of WSLOTS slice slots of (C, ny, nx)
+  float2* ws;     // ring of `slots` slice slots of (C, ny, nx), then the partial-sum ring
   int* sync;      // [0] ticket, [1..] cntA[S*C], cntB[S*C], cntC[S]
   int batch, ncoils;
+  int lagB, lagC, slots;  // schedule: round r = {A(r), B(r - lagB), C(r - lagC)}
   float mscale;
   const float4* coef;
   const float2* u;
@@ -103,9 +104,9 @@ struct FusedArgs {
 };
 
 // ---------------------------------------------------------------- A items
-template <int P, int QY, int QX>
+template <int P, int QY, int QX, int TILE>
 __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm) {
-  using F = FusedCfg<P, QY, QX>;
+  using F = FusedCfg<P, QY, QX, TILE>;
   using SX = typename F::SX;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
   const int tid = threadIdx.x;
@@ -146,7 +147,7 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm
   }
   __syncthreads();
   const int nrows = min(TILE, NY - rt * TILE);
-  float2* wj = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D + (long long)rt * TILE * NX;
+  float2* wj = a.ws + ((long long)(s % a.slots) * a.ncoils + j) * D + (long long)rt * TILE * NX;
   for (int e = tid; e < nrows * NX; e += T) {
     const int l3 = e / NX, pos = e - l3 * NX;
     st_ws(wj + e, buf[l3 * F::VSX + SX::pad(pos)], pol_evict_last());
@@ -154,9 +155,9 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm
 }
 
 // ---------------------------------------------------------------- B items
-template <int P, int QY, int QX>
+template <int P, int QY, int QX, int TILE>
 __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* sm) {
-  using F = FusedCfg<P, QY, QX>;
+  using F = FusedCfg<P, QY, QX, TILE>;
   using SY = typename F::SY;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
   const int tid = threadIdx.x;
@@ -168,7 +169,7 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   const float2* ty1 = sm + F::OFF_TY1;
   const float2* ty2 = sm + F::OFF_TY2;
   float2* buf = sm + F::OFF_BUF;
-  float2* img = a.ws + ((long long)(s % WSLOTS) * a.ncoils + j) * D;
+  float2* img = a.ws + ((long long)(s % a.slots) * a.ncoils + j) * D;
   float2 r[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q)
@@ -224,10 +225,10 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
 // partial ring, the last group to finish a row tile sums the G partials in a
 // fixed order (deterministic) and writes the epilogue.  Returns true when this
 // item finalised the row tile.
-template <int P, int QY, int QX>
+template <int P, int QY, int QX, int TILE>
 __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int CG, int* cntB,
                             int* cntT, int ncoltiles, float2* sm, int* s_flag) {
-  using F = FusedCfg<P, QY, QX>;
+  using F = FusedCfg<P, QY, QX, TILE>;
   using SX = typename F::SX;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
   const int tid = threadIdx.x;
@@ -238,7 +239,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
   const float2* tx2 = sm + F::OFF_TX2;
   float2* buf = sm + F::OFF_BUF;
   const int nrows = min(TILE, NY - rt * TILE);
-  const int slot = s % WSLOTS;
+  const int slot = s % a.slots;
   float2 acc[QX];
 #pragma unroll
   for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
@@ -279,7 +280,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
   }
   const long long roff = (long long)row * NX + p;
   if (G > 1) {
-    float2* part = a.ws + (long long)WSLOTS * a.ncoils * D + ((long long)slot * G + g) * D;
+    float2* part = a.ws + (long long)a.slots * a.ncoils * D + ((long long)slot * G + g) * D;
     if (valid) {
 #pragma unroll
       for (int q = 0; q < QX; ++q) st_ws(part + roff + P * q, acc[q], pol_evict_last());
@@ -288,7 +289,7 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
     if (tid == 0) *s_flag = (atom_add_acqrel(cntT + s * ((NY + TILE - 1) / TILE) + rt, 1) == G - 1);
     __syncthreads();
     if (!*s_flag) return false;
-    const float2* pb = a.ws + (long long)WSLOTS * a.ncoils * D + (long long)slot * G * D;
+    const float2* pb = a.ws + (long long)a.slots * a.ncoils * D + (long long)slot * G * D;
 #pragma unroll
     for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
     if (valid) {
@@ -319,114 +320,117 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
 // ---------------------------------------------------------------- scheduler
 constexpr int COILS_PER_C = 3;  // coils per C item (partial coil sums, G = ceil(C / 3) groups)
 
-template <int P, int QY, int QX>
-__global__ void __launch_bounds__(FusedCfg<P, QY, QX>::T, 2)
+template <int P, int QY, int QX, int TILE>
+__global__ void __launch_bounds__(FusedCfg<P, QY, QX, TILE>::T, (TILE >= 16 ? 2 : 4))
 k_cart_normal_fused(FusedArgs a) {
-  using F = FusedCfg<P, QY, QX>;
+  using F = FusedCfg<P, QY, QX, TILE>;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
   extern __shared__ __align__(16) float2 sm[];
   __shared__ int s_ticket, s_flag;
   const int tid = threadIdx.x;
-  init_tw_s1<P, QX>(sm + F::OFF_TX1, tid, T);
-  init_tw_s2<P, QX>(sm + F::OFF_TX2, tid, T);
-  init_tw_s1<P, QY>(sm + F::OFF_TY1, tid, T);
-  init_tw_s2<P, QY>(sm + F::OFF_TY2, tid, T);
-  __syncthreads();
   const int S = a.batch, C = a.ncoils;
   const int nrt = (NY + TILE - 1) / TILE, nct = (NX + TILE - 1) / TILE;
   const int G = (C + COILS_PER_C - 1) / COILS_PER_C;
   const int nA = nrt * C, nB = nct * C, nC = nrt * G;
+  const int LB = a.lagB, LC = a.lagC;
+  const int R = S + LC;  // rounds
+  int* rstart = reinterpret_cast<int*>(sm + F::OFF_BUF + F::BUF);  // R + 1 round offsets
+  init_tw_s1<P, QX>(sm + F::OFF_TX1, tid, T);
+  init_tw_s2<P, QX>(sm + F::OFF_TX2, tid, T);
+  init_tw_s1<P, QY>(sm + F::OFF_TY1, tid, T);
+  init_tw_s2<P, QY>(sm + F::OFF_TY2, tid, T);
+  if (tid == 0) {
+    int acc = 0;
+    for (int r = 0; r < R; ++r) {
+      rstart[r] = acc;
+      acc += (r < S ? nA : 0) + (r >= LB && r < S + LB ? nB : 0) + (r >= LC ? nC : 0);
+    }
+    rstart[R] = acc;
+  }
+  __syncthreads();
+  const int total = rstart[R];
   int* cntA = a.sync + 1;
   int* cntB = cntA + S * C;
   int* cntC = cntB + S * C;     // finalised row tiles per slice
   int* cntT = cntC + S;         // finished coil groups per (slice, row tile)
-  const long long total = (long long)S * (nA + nB + nC);
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(a.sync, 1);
     __syncthreads();
-    long long t = s_ticket;
+    const int t = s_ticket;
     __syncthreads();
     if (t >= total) break;
-    // round r holds A(r) [r < S], B(r-1) [1 <= r <= S], C(r-2) [2 <= r <= S+1]
-    int r = 0;
-    if (S >= 3) {  // closed form: rounds 2..S-1 are full
-      const long long full = nA + nB + nC;
-      if (t < nA) {
-        r = 0;
-      } else if ((t -= nA) < nA + nB) {
-        r = 1;
-      } else {
-        t -= nA + nB;
-        const long long k = t / full;
-        if (k < S - 2) {
-          r = 2 + (int)k;
-          t -= k * full;
-        } else {
-          t -= (long long)(S - 2) * full;
-          if (t < nB + nC) r = S;
-          else { r = S + 1; t -= nB + nC; }
-        }
-      }
-    } else {
-      for (;; ++r) {
-        const long long sz = (r < S ? nA : 0) + (r >= 1 && r <= S ? nB : 0) + (r >= 2 && r <= S + 1 ? nC : 0);
-        if (t < sz) break;
-        t -= sz;
-      }
+    // round = last r with rstart[r] <= t (binary search)
+    int lo = 0, hi = R - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rstart[mid] <= t) lo = mid; else hi = mid - 1;
     }
-    const int it = (int)t;
+    const int r = lo;
+    int it = t - rstart[r];
     if (r < S && it < nA) {
       const int s = r, rt = it % nrt, j = it / nrt;
-      if (s >= WSLOTS) {  // slot reuse: every row tile of slice s - WSLOTS is final
+      if (s >= a.slots) {  // slot reuse: every row tile of slice s - slots is final
         if (tid == 0) {
-          const int* c = cntC + (s - WSLOTS);
+          const int* c = cntC + (s - a.slots);
           while (ld_acquire(c) < nrt) __nanosleep(64);
         }
         __syncthreads();
       }
-      item_rowfwd<P, QY, QX>(a, s, rt, j, sm);
+      item_rowfwd<P, QY, QX, TILE>(a, s, rt, j, sm);
       __syncthreads();
       if (tid == 0) red_release_add(cntA + s * C + j, 1);
-    } else {
-      const int it2 = it - (r < S ? nA : 0);
-      if (r >= 1 && r <= S && it2 < nB) {
-        const int s = r - 1, ct = it2 % nct, j = it2 / nct;
-        if (tid == 0) {
-          const int* c = cntA + s * C + j;
-          while (ld_acquire(c) < nrt) __nanosleep(64);
-        }
-        __syncthreads();
-        item_colpass<P, QY, QX>(a, s, ct, j, sm);
-        __syncthreads();
-        if (tid == 0) red_release_add(cntB + s * C + j, 1);
-      } else {
-        const int it3 = it2 - (r >= 1 && r <= S ? nB : 0);
-        const int s = r - 2, rt = it3 % nrt, g = it3 / nrt;
-        const bool fin = item_rowinv<P, QY, QX>(a, s, rt, g, G, COILS_PER_C, cntB, cntT, nct, sm, &s_flag);
-        __syncthreads();
-        if (fin && tid == 0) red_release_add(cntC + s, 1);
+      continue;
+    }
+    if (r < S) it -= nA;
+    if (r >= LB && r < S + LB && it < nB) {
+      const int s = r - LB, ct = it % nct, j = it / nct;
+      if (tid == 0) {
+        const int* c = cntA + s * C + j;
+        while (ld_acquire(c) < nrt) __nanosleep(64);
       }
+      __syncthreads();
+      item_colpass<P, QY, QX, TILE>(a, s, ct, j, sm);
+      __syncthreads();
+      if (tid == 0) red_release_add(cntB + s * C + j, 1);
+      continue;
+    }
+    if (r >= LB && r < S + LB) it -= nB;
+    {
+      const int s = r - LC, rt = it % nrt, g = it / nrt;
+      const bool fin = item_rowinv<P, QY, QX, TILE>(a, s, rt, g, G, COILS_PER_C, cntB, cntT, nct, sm, &s_flag);
+      __syncthreads();
+      if (fin && tid == 0) red_release_add(cntC + s, 1);
     }
     __syncthreads();
   }
 }
 
-template <int P, int QY, int QX>
-int launch_fused(const FusedArgs& a, cudaStream_t st) {
-  using F = FusedCfg<P, QY, QX>;
-  static int grid = 0;
-  if (grid == 0) {
-    if (cudaFuncSetAttribute(k_cart_normal_fused<P, QY, QX>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F::SMEM) != cudaSuccess)
+struct FusedConfig {
+  int lagB = 1, lagC = 2, slots = 4, tile = 16;
+};
+FusedConfig g_cfg;
+
+template <int P, int QY, int QX, int TILE>
+int launch_fused(FusedArgs a, cudaStream_t st) {
+  using F = FusedCfg<P, QY, QX, TILE>;
+  static int per = 0, nsm = 0;
+  const size_t smem = F::SMEM + sizeof(int) * (a.batch + a.lagC + 2);
+  static size_t configured = 0;
+  if (smem > configured) {
+    if (cudaFuncSetAttribute(k_cart_normal_fused<P, QY, QX, TILE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SR_ECUDA;
-    int dev = 0, nsm = 0, per = 0;
+    configured = smem;
+    per = 0;
+  }
+  if (per == 0) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cart_normal_fused<P, QY, QX>, F::T, F::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cart_normal_fused<P, QY, QX, TILE>, F::T, smem);
     if (per < 1) return SR_ECUDA;
-    grid = nsm * per;
   }
-  k_cart_normal_fused<P, QY, QX><<<grid, F::T, F::SMEM, st>>>(a);
+  k_cart_normal_fused<P, QY, QX, TILE><<<nsm * per, F::T, smem, st>>>(a);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -445,25 +449,41 @@ int sr_fused_normal_supported(int ny, int nx) {
   return 0;
 }
 
+static int fused_tile(int ny, int nx) {
+  (void)ny; (void)nx;
+  return g_cfg.tile;
+}
+
 long long sr_fused_sync_ints(int batch, int ncoils, int ny) {
-  return 1 + 2LL * batch * ncoils + batch + (long long)batch * ((ny + TILE - 1) / TILE);
+  return 1 + 2LL * batch * ncoils + batch + (long long)batch * ((ny + 7) / 8);
 }
 // complex64 elements of workspace: coil ring + partial-sum ring
 long long sr_fused_ws_elems(int batch, int ncoils, long long D) {
   const long long G = (ncoils + COILS_PER_C - 1) / COILS_PER_C;
-  return (long long)WSLOTS * ncoils * D + (G > 1 ? (long long)WSLOTS * G * D : 0);
+  const long long slots = batch < g_cfg.slots ? batch : g_cfg.slots;
+  return slots * ncoils * D + (G > 1 ? slots * G * D : 0);
+}
+
+extern "C" int sr_fused_config(int lagB, int lagC, int slots, int tile) {
+  if (lagB < 1 || lagC <= lagB || slots < lagC + 1 || slots > MAX_SLOTS || (tile != 8 && tile != 16))
+    return SR_EINVAL;
+  g_cfg.lagB = lagB; g_cfg.lagC = lagC; g_cfg.slots = slots; g_cfg.tile = tile;
+  return SR_OK;
 }
 
 int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
                     const uint8_t* maskT, long long mask_bstride, float2* out, float2* ws, int* sync,
                     int batch, int ncoils, int ny, int nx, const float4* coef, const float2* u,
                     const float2* d, cudaStream_t st) {
+  const int slots = batch < g_cfg.slots ? batch : g_cfg.slots;
   FusedArgs a{x, anchor, maps, map_bstride, maskT, mask_bstride, out, ws, sync, batch, ncoils,
-              (float)(1.0 / ((double)ny * nx)), coef, u, d};
+              g_cfg.lagB, g_cfg.lagC, slots < 1 ? 1 : slots, (float)(1.0 / ((double)ny * nx)), coef, u, d};
   if (cudaMemsetAsync(sync, 0, sizeof(int) * sr_fused_sync_ints(batch, ncoils, ny), st) != cudaSuccess)
     return SR_ECUDA;
-#define X(P, QY, QX) \
-  if (ny == P * QY && nx == P * QX) return launch_fused<P, QY, QX>(a, st);
+  const int tile = fused_tile(ny, nx);
+#define X(P, QY, QX)                                                        \
+  if (ny == P * QY && nx == P * QX)                                         \
+    return tile == 8 ? launch_fused<P, QY, QX, 8>(a, st) : launch_fused<P, QY, QX, 16>(a, st);
   SR_FUSED_SIZES(X)
 #undef X
   return SR_EUNSUPPORTED;

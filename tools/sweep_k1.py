@@ -22,12 +22,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--chunks", default="0,32,16,8,4,2,1")
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--fused", default="", help="semicolon list of lagB,lagC,slots,tile configs for chunk 0")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     w = bench.build_workload(0, dev)
     kern, smaps, x = w["kern"], w["smaps"], w["x"]
     out = torch.empty_like(x)
-    for ch in [int(c) for c in args.chunks.split(",")]:
+    from paper_2305_06482_b200 import _lib
+    for cfg in [c for c in args.fused.split(";") if c]:
+        lb, lc, sl, tl = (int(v) for v in cfg.split(","))
+        _lib.call("sr_fused_config", lb, lc, sl, tl)
+        kern._ws = None
+        t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=0), args.steps, 3, torch.cuda.synchronize)
+        ms = t / args.steps * 1e3
+        print(json.dumps({"fused": cfg, "ms_per_apply": ms,
+                          "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}), flush=True)
+    for ch in [int(c) for c in args.chunks.split(",") if c]:
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=ch), args.steps, 3, torch.cuda.synchronize)
         ms = t / args.steps * 1e3
         print(json.dumps({"chunk": ch, "ms_per_apply": ms,
