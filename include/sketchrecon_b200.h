@@ -53,9 +53,10 @@ int sr_fft_split(int n, int* P, int* Q);
  *   anchor: NULL or (batch, ny, nx): operator input is x - anchor
  *   coef: NULL -> out = acc; else device float4 per slice {s_acc, s_u, s_d, -}:
  *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v)
- *   chunk: 0 = auto: the single persistent fused launch (cart_fused.cu) when
- *          sr_fused_normal_supported(ny, nx), else three launches over the batch;
- *          > 0: three launches per group of `chunk` slices; -1: three launches, whole batch.
+ *   chunk: 0 = three launches (row FFT, column FFT-mask-IFFT, row IFFT + coil sum)
+ *          over the whole batch; > 0: the three launches per group of `chunk` slices;
+ *          -1: one persistent launch with an L2-resident workspace ring (cart_fused.cu,
+ *          sizes with sr_fused_normal_supported)
  *   ws: sr_cart_ws_bytes(batch, ncoils, ny, nx, chunk) bytes */
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,

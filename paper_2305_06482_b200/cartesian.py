@@ -59,7 +59,7 @@ class CartesianKernel:
         woff[1:] = np.cumsum([len(p.wlist) for p in per_slice])
         self.woff = dv.host_to_dev(woff, torch.int64, dev)
         self._ws = None
-        self.chunk = 0  # sr_cart_normal schedule: 0 auto (fused), >0 chunked 3-pass, -1 3-pass
+        self.chunk = 0  # sr_cart_normal schedule: 0 three launches, >0 chunked, -1 persistent fused
         self._plans = plans
         self._replicas: dict[int, "CartesianKernel"] = {}
 
@@ -94,9 +94,8 @@ class CartesianKernel:
     def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None, chunk=None):
         """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1).
 
-        chunk: None -> self.chunk; 0 -> auto (single persistent fused launch when the grid
-        has an instantiation); > 0 -> three launches per group of `chunk` slices; -1 -> three
-        launches over the whole batch.
+        chunk: None -> self.chunk; 0 -> three launches over the batch; > 0 -> three launches
+        per group of `chunk` slices; -1 -> one persistent launch (L2-resident workspace ring).
         """
         _no_weights(w)
         ncoils, mbs = self._maps_stride(maps)

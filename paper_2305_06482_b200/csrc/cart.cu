@@ -470,7 +470,7 @@ int sr_fft_split(int n, int* P, int* Q) {
 
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk) {
   const long long D = (long long)ny * nx;
-  if (chunk == 0 && sr_fused_normal_supported(ny, nx))
+  if (chunk == -1 && sr_fused_normal_supported(ny, nx))
     return 8LL * sr_fused_ws_elems(batch, ncoils, D) + 4LL * sr_fused_sync_ints(batch, ncoils, ny) + 256;
   const int nb = (chunk <= 0 || chunk > batch) ? batch : chunk;
   return 8LL * nb * ncoils * D;
@@ -482,7 +482,8 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk, void* stream) {
   if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < -1) return SR_EINVAL;
   if (!fft_size_supported(nx) || !fft_size_supported(ny)) return SR_EUNSUPPORTED;
-  if (chunk == 0 && sr_fused_normal_supported(ny, nx)) {
+  if (chunk == -1) {
+    if (!sr_fused_normal_supported(ny, nx)) return SR_EUNSUPPORTED;
     const long long D = (long long)ny * nx;
     int* sync = (int*)((float2*)ws + sr_fused_ws_elems(batch, ncoils, D));
     return sr_fused_normal((const float2*)x, (const float2*)anchor, (const float2*)maps, map_bstride,

@@ -102,9 +102,18 @@ def test_batched_normal_op_vs_oracle(cuda, dims):
     out = torch.empty_like(xd)
     kern.normal(md, xd, out)
     got = out.cpu().numpy()
+    refs = [O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b])).normal(x[b]) for b in range(B)]
     for b in range(B):
-        ref = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b])).normal(x[b])
-        assert rel(got[b], ref) < OP_TOL, b
+        assert rel(got[b], refs[b]) < OP_TOL, b
+    # the other schedules of the same operator: chunked three-pass and the persistent launch
+    from paper_2305_06482_b200 import _lib
+    schedules = [2] + ([-1] if _lib.lib().sr_fused_normal_supported(*dims) else [])
+    for ch in schedules:
+        out2 = torch.full_like(xd, float("nan"))
+        kern.normal(md, xd, out2, chunk=ch)
+        got2 = out2.cpu().numpy()
+        for b in range(B):
+            assert rel(got2[b], refs[b]) < OP_TOL, (ch, b)
     # forward / adjoint with ragged per-slice samples
     y = kern.forward(md, xd)
     for b in range(B):
