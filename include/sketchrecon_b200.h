@@ -140,6 +140,36 @@ int sr_lincomb(sr_c64* out, const sr_c64* X, const sr_c64* Y, const sr_c64* Z,
 int sr_scalar_op(int op, const double* in0, const double* in1, double* state, float* coefA,
                  float* coefB, int* flags, int batch, void* stream);
 
+/* K3/K4 -- Kaiser-Bessel gridded NUFFT SENSE operator, 2-D or 3-D, one image
+ * (replaces _GriddedNUFFTKernel.apply/apply_adjoint, linops.py:494-516, inside
+ * SenseOperator with density weights, forward_model.py:168-180).
+ *   dims/gdims: 3 image / oversampled-grid dims (leading 1 for 2-D); betas: 3 KB betas
+ *   (dims, gdims, betas are HOST arrays, every other pointer is a device pointer);
+ *   ia0..ia2: inverse apodisation per axis (fp32 of the fp64 reference formula);
+ *   base (3, N) int32 = ceil(u - w/2) per axis (fp64 on the host), frac (3, N) fp32 = u - base;
+ *   wgt: w (normal) or sqrt(w) (forward / adjoint) per sample, NULL = 1; orig: original
+ *   index of each (locality-sorted) sample or NULL; grids: ncoils*G (fwd/adj) or
+ *   2*ncoils*G (normal) complex64 workspace.  Epilogue coef/u/d as sr_cart_normal. */
+int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
+                    const int* dims, const int* gdims, const float* betas, int width,
+                    const float* ia0, const float* ia1, const float* ia2, const int* base,
+                    const float* frac, const float* wgt, long long nsamples, sr_c64* out,
+                    sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int* dims, const int* gdims,
+                     const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
+                     const int* base, const float* frac, const float* sqrtw, const int* orig,
+                     long long nsamples, sr_c64* y, const sr_c64* ymeas, double* partial, sr_c64* grids,
+                     void* stream);
+int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int* dims, const int* gdims,
+                     const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
+                     const int* base, const float* frac, const float* sqrtw, const int* orig,
+                     long long nsamples, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
+                     const sr_c64* d, void* stream);
+int sr_nufft_partial_blocks(long long nsamples);
+/* Batched unnormalised FFT along the middle axis of an [outer][n][inner] array, in
+ * place: inv = 0 natural -> perm order, inv = 1 perm -> natural. */
+int sr_fft_axis(sr_c64* data, long long outer, int n, long long inner, int inv, void* stream);
+
 /* Host (CPU) synthetic-input helper: variable-density Poisson-disc mask of
  * ny x nx bins (1 = sampled, row-major) with a fully sampled calib x calib
  * centre and about ny*nx/accel samples (BASELINE configs 0-2; the reference

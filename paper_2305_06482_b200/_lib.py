@@ -38,6 +38,14 @@ SIGNATURES = {
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
     "sr_fused_normal_supported": [_i, _i],
     "sr_fused_config": [_i, _i, _i, _i],
+    "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
+                        _vp, _vp, _vp, _vp],
+    "sr_nufft_forward": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
+                         _vp, _vp, _vp],
+    "sr_nufft_adjoint": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
+                         _vp, _vp, _vp, _vp],
+    "sr_nufft_partial_blocks": [_ll],
+    "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
 }
 RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong}
 

@@ -108,6 +108,10 @@ class CartesianKernel:
                   ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), chunk, dv.stream())
         return out
 
+    def partial_shape(self, ncoils: int) -> tuple:
+        """Shape of the residual partial-sum buffer `forward(partial=...)` fills."""
+        return (self.batch, ncoils, 64)
+
     def forward(self, maps, x, y=None, *, ymeas=None, partial=None, partial_blocks=64, w=None):
         """y[b, j, :N_b] = A_b x_b  (- ymeas);  partial sums of |y|^2 if requested (K2)."""
         _no_weights(w)

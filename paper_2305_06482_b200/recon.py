@@ -81,8 +81,7 @@ class SketchedReconEngine:
         mk = lambda: torch.zeros(B, D, dtype=torch.complex64, device=self.dev)  # noqa: E731
         self.x, self.z, self.v, self.d, self.anchor = mk(), mk(), mk(), mk(), mk()
         self.r = torch.zeros_like(self.y)
-        self.nparts = 64
-        self.partial = torch.zeros(B, self.C0, self.nparts, dtype=torch.float64, device=self.dev)
+        self.partial = torch.zeros(kernel.partial_shape(self.C0), dtype=torch.float64, device=self.dev)
         self.step = None       # (B,) float64 device
         self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
         self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
@@ -93,9 +92,8 @@ class SketchedReconEngine:
 
     def objective(self, x) -> torch.Tensor:
         """Per-slice 0.5||A x - y||^2 + g(x) (float64 device); leaves A x - y in self.r."""
-        self.kernel.forward(self.maps0, x, self.r, ymeas=self.y, partial=self.partial,
-                            partial_blocks=self.nparts, w=self.sqrt_w)
-        obj = 0.5 * self.partial.sum(dim=(1, 2))
+        self.kernel.forward(self.maps0, x, self.r, ymeas=self.y, partial=self.partial, w=self.sqrt_w)
+        obj = 0.5 * self.partial.reshape(self.B, -1).sum(dim=1)
         if self.lam != 0.0:
             if self.reg == "l1-wavelet":
                 obj = obj + self.lam * self.wav.l1_norm(x)

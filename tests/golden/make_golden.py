@@ -144,7 +144,7 @@ def main():
                          batch=b, y=yy, fwd=kern.apply(b), adj=kern.apply_adjoint(yy), weights=wts,
                          maps=maps, x=xx, AHAx=a.adjoint(a.forward(xx)))
     # 3-D gridded NUFFT
-    dims = (8, 10, 6)
+    dims = (8, 12, 6)
     shape = lo.GridShape(dims)
     pts = np.stack([g.uniform(-n / 2, n / 2 - 1e-6, 60) for n in dims], axis=1)
     traj = lo.Trajectory(pts, "non-cartesian")

@@ -189,3 +189,74 @@ def test_coil_sketching_recon_matches_reference(cuda, name, solver, kind):
     np.testing.assert_allclose([r.objective for r in rep.per_outer], g["objectives"], rtol=1e-4)
     assert rep.counts["coil_transform"] == int(g["counts"]) == int(g["expected"])
     assert rep.diverged == bool(g["diverged"])
+
+
+# ----------------------------------------------------------------------------- NUFFT (K3/K4)
+@pytest.mark.parametrize("name", ["nufft_2x_w4", "nufft_125_w4", "nufft_125_w6", "nufft3d"])
+def test_gridded_nufft_kernel_matches_reference(cuda, name):
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    g = golden(name)
+    dims = tuple(int(n) for n in g["dims"])
+    k = GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    assert k.n_points == len(g["points"])
+    assert rel(k.apply(g["batch"]), g["fwd"]) < OP_TOL
+    assert rel(k.apply_adjoint(g["y"]), g["adj"]) < OP_TOL
+
+
+@pytest.mark.parametrize("name", ["nufft_2x_w4", "nufft_125_w4", "nufft_125_w6"])
+def test_nufft_sense_normal_with_density_weights(cuda, name):
+    cs, fm, lo, sk, so = _api()
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    g = golden(name)
+    dims = tuple(int(n) for n in g["dims"])
+    shape = lo.GridShape(dims)
+    traj = lo.Trajectory(g["points"], "non-cartesian")
+    w = fm.radial_density_weights(traj)
+    assert rel(w.w, g["weights"]) < 1e-14
+    kern = GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    a = fm.SenseOperator(fm.SensitivityMaps(shape, g["maps"]), traj, w, kernel=kern)
+    assert rel(a.adjoint(a.forward(g["x"])), g["AHAx"]) < OP_TOL
+    x = torch.from_numpy(g["x"].astype(np.complex64)).cuda().view(1, -1)
+    out = torch.empty_like(x)
+    a.normal_into(x, out)
+    assert rel(out.cpu().numpy().ravel(), g["AHAx"]) < OP_TOL
+
+
+def test_nufft_large_2d_vs_oracle(cuda):
+    """config-3 geometry (320^2, 2x grid, w4, 128 golden-angle spokes x 640) against the oracle."""
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    dims = (320, 320)
+    pts = synth.golden_angle_radial(128, 640, dims)
+    rng = np.random.default_rng(11)
+    maps = synth.gaussian_coil_maps(dims, 3, rng)
+    x = synth.random_ellipses(dims, 6, rng).ravel()
+    w = O.radial_density_weights(pts)
+    ok = O.GriddedKernel(dims, pts, 2.0, 4)
+    ref = O.Sense(maps, ok, w).normal(x)
+    kern = GriddedKernel(dims, pts, 2.0, 4)
+    md = torch.from_numpy(maps.astype(np.complex64)).cuda().unsqueeze(0)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda().view(1, -1)
+    sw = torch.from_numpy(np.sqrt(w)).cuda()
+    out = torch.empty_like(xd)
+    kern.normal(md, xd, out, w=sw)
+    assert rel(out.cpu().numpy().ravel(), ref) < OP_TOL
+    y = kern.forward(md, xd, w=sw)
+    assert rel(y.cpu().numpy().ravel(), O.Sense(maps, ok, w).forward(x)) < OP_TOL
+
+
+def test_coil_sketching_recon_radial_matches_reference(cuda):
+    g = golden("recon_radial")
+    cs, fm, lo, sk, so, dims, shape, traj, nufft = _recon_inputs(g)
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    reg = so.make_regularizer("l1-wavelet", float(g["lam"]), shape)
+    v, s = int(g["v"]), int(g["s"])
+    cfg = cs.CoilSketchConfig(int(g["chat0"]), sk.SketchConfig(v + s, v, s, rademacher_scale=float(g["scale"])),
+                              reg, int(g["outer"]), int(g["inner"]))
+    kern = GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    rep = cs.coil_sketching_recon(fm.KSpaceData(traj, g["data"]), fm.SensitivityMaps(shape, g["maps"]), cfg,
+                                  weights=fm.DensityWeights(g["weights"]), kernel=kern)
+    x, ref = rep.x_final.values, g["x_final"]
+    assert np.linalg.norm(np.abs(x) - np.abs(ref)) / np.linalg.norm(ref) <= IMG_TOL
+    np.testing.assert_allclose([r.objective for r in rep.per_outer], g["objectives"], rtol=1e-4)
+    assert rep.counts["coil_transform"] == int(g["counts"])
