@@ -572,9 +572,9 @@ int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int*
   SR_CHECK_LAUNCH();
   int rc = grid_fft(dst, g, ncoils, 1, st);
   if (rc) return rc;
+  // the 1/sqrt(D) scale was applied with the spread
   k_nufft_crop<<<148 * 8, 256, 0, st>>>(dst, (const float2*)maps, ia0, ia1, ia2, (float2*)out, g, ncoils,
-                                        (float)(1.0 / sqrt((double)g.D)), (const float4*)coef,
-                                        (const float2*)u, (const float2*)d);
+                                        1.f, (const float4*)coef, (const float2*)u, (const float2*)d);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
