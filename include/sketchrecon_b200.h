@@ -170,6 +170,13 @@ int sr_nufft_partial_blocks(long long nsamples);
  * place: inv = 0 natural -> perm order, inv = 1 perm -> natural. */
 int sr_fft_axis(sr_c64* data, long long outer, int n, long long inner, int inv, void* stream);
 
+/* K8 -- readout decoupling of 3-D Cartesian data (BASELINE config 2): centered unitary
+ * IDFT along the fully sampled readout of in (ncoils, n, inner), written slice-major to
+ * out (n, ncoils, inner); pre[k], post[x] (device, length n) carry the centering phases
+ * and n^-1/2 (host-computed in fp64).  Each out[x] is then the 2-D SENSE data of slice x. */
+int sr_readout_idft(const sr_c64* in, sr_c64* out, const sr_c64* pre, const sr_c64* post, int ncoils, int n,
+                    long long inner, void* stream);
+
 /* Host (CPU) synthetic-input helper: variable-density Poisson-disc mask of
  * ny x nx bins (1 = sampled, row-major) with a fully sampled calib x calib
  * centre and about ny*nx/accel samples (BASELINE configs 0-2; the reference

@@ -46,6 +46,7 @@ SIGNATURES = {
                          _vp, _vp, _vp, _vp],
     "sr_nufft_partial_blocks": [_ll],
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
+    "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],
 }
 RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong}
 

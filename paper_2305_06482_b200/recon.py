@@ -56,11 +56,20 @@ class SketchedReconEngine:
     def __init__(self, kernel, maps0: torch.Tensor, y: torch.Tensor, *, dims, sketch: SketchConfig,
                  lam: float, reg: str = "l1-wavelet", solver: str = "fista", step_scale: float = 0.9,
                  sqrt_w: torch.Tensor | None = None, wavelet_levels: int | None = None,
-                 counter: CostCounter | None = None):
+                 counter: CostCounter | None = None, shard=None):
         self.kernel = kernel
-        self.maps0 = maps0.contiguous()          # (B, C0, D)
+        self.maps0 = maps0.contiguous()          # (B, C0, D) all compressed coils (sketch input)
         self.B, self.C0, self.D = self.maps0.shape
-        self.y = y.contiguous()                  # (B, C0, nmax) weighted measurements
+        # coil sharding (config 4): this rank applies the full operator over its coil block and
+        # the sketched operator over its block of sketched coils; partials are all-reduced
+        self.shard = shard if (shard is not None and shard.world > 1) else None
+        if self.shard is not None:
+            lo, hi = self.shard.coils(self.C0)
+            self.maps_full = self.maps0[:, lo:hi].contiguous()
+            y = y[:, lo:hi]
+        else:
+            self.maps_full = self.maps0
+        self.y = y.contiguous()                  # (B, C0 or local coils, nmax) weighted measurements
         self.sketch = sketch
         self.lam = float(lam)
         self.reg = reg
@@ -81,18 +90,47 @@ class SketchedReconEngine:
         mk = lambda: torch.zeros(B, D, dtype=torch.complex64, device=self.dev)  # noqa: E731
         self.x, self.z, self.v, self.d, self.anchor = mk(), mk(), mk(), mk(), mk()
         self.r = torch.zeros_like(self.y)
-        self.partial = torch.zeros(kernel.partial_shape(self.C0), dtype=torch.float64, device=self.dev)
+        self.partial = torch.zeros(kernel.partial_shape(max(1, self.maps_full.shape[1])), dtype=torch.float64,
+                                   device=self.dev)
+        self.tmp = mk() if self.shard is not None else None
         self.step = None       # (B,) float64 device
         self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
         self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
 
     # ------------------------------------------------------------ pieces
-    def _normal(self, maps, x, out, **kw):
-        return self.kernel.normal(maps, x, out, w=self.sqrt_w, **kw)
+    def _normal(self, maps, x, out, anchor=None, coef=None, u=None, d=None):
+        if self.shard is None:
+            return self.kernel.normal(maps, x, out, w=self.sqrt_w, anchor=anchor, coef=coef, u=u, d=d)
+        # partial over this rank's sketched coils, all-reduce, then the epilogue
+        if maps.shape[1] > 0:
+            self.kernel.normal(maps, x, self.tmp, w=self.sqrt_w, anchor=anchor)
+        else:
+            self.tmp.zero_()
+        self.shard.all_reduce_(self.tmp)
+        if coef is None:
+            out.copy_(self.tmp)
+        else:
+            _lib.call("sr_lincomb", dv.ptr(out), dv.ptr(self.tmp), dv.ptr(u), dv.ptr(d), dv.ptr(coef), 0.0, 0.0,
+                      0.0, self.D, self.D, self.B, dv.stream())
+        return out
+
+    def _sketch(self, mat: np.ndarray) -> torch.Tensor:
+        """This rank's rows of S^t @ maps0 (all rows without sharding)."""
+        if self.shard is None:
+            return coil_contract(self.maps0, mat)
+        lo, hi = self.shard.coils(mat.shape[0])
+        if hi == lo:
+            return torch.zeros(self.B, 0, self.D, dtype=torch.complex64, device=self.dev)
+        return coil_contract(self.maps0, mat[lo:hi])
 
     def objective(self, x) -> torch.Tensor:
         """Per-slice 0.5||A x - y||^2 + g(x) (float64 device); leaves A x - y in self.r."""
-        self.kernel.forward(self.maps0, x, self.r, ymeas=self.y, partial=self.partial, w=self.sqrt_w)
+        if self.maps_full.shape[1] > 0:
+            self.kernel.forward(self.maps_full, x, self.r, ymeas=self.y, partial=self.partial, w=self.sqrt_w)
+        else:
+            self.partial.zero_()
+        if self.shard is not None:
+            self.shard.all_reduce_(self.partial)
         obj = 0.5 * self.partial.reshape(self.B, -1).sum(dim=1)
         if self.lam != 0.0:
             if self.reg == "l1-wavelet":
@@ -104,7 +142,12 @@ class SketchedReconEngine:
     def true_gradient(self, out):
         """d = A^H r with r = A x - y from the last objective (coil_sketch.py:123-126)."""
         self.counter.add("coil_transform", 2 * self.C0)
-        self.kernel.adjoint(self.maps0, self.r, out, w=self.sqrt_w)
+        if self.maps_full.shape[1] > 0:
+            self.kernel.adjoint(self.maps_full, self.r, out, w=self.sqrt_w)
+        else:
+            out.zero_()
+        if self.shard is not None:
+            self.shard.all_reduce_(out)
         return out
 
     def power_lambda(self, smaps, iters: int = 30, seed: int = 0) -> torch.Tensor:
@@ -138,7 +181,7 @@ class SketchedReconEngine:
         self.z.copy_(self.anchor)
         t_k = 1.0
         for _ in range(inner):
-            self.counter.add("coil_transform", 2 * smaps.shape[1])
+            self.counter.add("coil_transform", 2 * self.chat)
             # v = z - step * (A_s^H A_s (z - anchor) + d)
             self._normal(smaps, self.z, self.v, anchor=self.anchor, coef=self.fcoef, u=self.z, d=self.d)
             t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_k * t_k))
@@ -177,7 +220,7 @@ class SketchedReconEngine:
         lcoef[:, 0] = 1.0
         lcoef[:, 1] = self.lam
         for _ in range(inner):
-            self.counter.add("coil_transform", 2 * smaps.shape[1])
+            self.counter.add("coil_transform", 2 * self.chat)
             self._normal(smaps, p, mp, coef=lcoef, u=p)
             _lib.call("sr_reduce", 1, dv.ptr(p), dv.ptr(mp), D, D, B, dv.ptr(part), dv.ptr(den), st)
             _lib.call("sr_scalar_op", 1, None, dv.ptr(den), dv.ptr(state), dv.ptr(cA), dv.ptr(cB), None, B, st)
@@ -210,7 +253,8 @@ class SketchedReconEngine:
         for t in range(1, outer + 1):
             self.true_gradient(self.d)
             sk = gen_sketch_matrix(self.sketch.with_seed(child_seed(self.sketch.seed, t)), self.C0)
-            smaps = coil_contract(self.maps0, sk.mat)
+            self.chat = sk.mat.shape[0]
+            smaps = self._sketch(sk.mat)
             if self.solver == "fista" and lip is None:
                 lam_max = self.power_lambda(smaps)
                 lip = lam_max / self.step_scale

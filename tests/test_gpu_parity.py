@@ -260,3 +260,57 @@ def test_coil_sketching_recon_radial_matches_reference(cuda):
     assert np.linalg.norm(np.abs(x) - np.abs(ref)) / np.linalg.norm(ref) <= IMG_TOL
     np.testing.assert_allclose([r.objective for r in rep.per_outer], g["objectives"], rtol=1e-4)
     assert rep.counts["coil_transform"] == int(g["counts"])
+
+
+# ----------------------------------------------------------------------------- config 2 path
+def test_readout_decoupling_matches_3d_reference_convention(cuda):
+    """K8: centered IDFT along the readout of 3-D Cartesian data == per-slice 2-D SENSE data,
+    with the 3-D data produced by the oracle's 3-D Cartesian operator (argwhere order, kx-major)."""
+    from paper_2305_06482_b200.parallel_recon import ReadoutDecoupler
+    rng = np.random.default_rng(4)
+    nx, ny, nz, C = 16, 12, 10, 3
+    m2 = rng.random((ny, nz)) < 0.4
+    m3 = np.broadcast_to(m2, (nx, ny, nz))
+    pts3 = np.argwhere(m3) - np.array([nx // 2, ny // 2, nz // 2])
+    maps = (rng.standard_normal((C, nx, ny, nz)) + 1j * rng.standard_normal((C, nx, ny, nz))) / 2
+    vol = rng.standard_normal((nx, ny, nz)) + 1j * rng.standard_normal((nx, ny, nz))
+    k3 = O.Sense(maps.reshape(C, -1), O.CartesianKernel((nx, ny, nz), pts3)).forward(vol.ravel())
+    k3 = k3.reshape(C, nx, -1)
+    dec = ReadoutDecoupler(nx)
+    got = dec(torch.from_numpy(k3.astype(np.complex64)).cuda()).cpu().numpy()  # (nx, C, Nyz)
+    pts2 = np.argwhere(m2) - np.array([ny // 2, nz // 2])
+    for x in range(nx):
+        ref = O.Sense(maps[:, x].reshape(C, -1), O.CartesianKernel((ny, nz), pts2)).forward(vol[x].ravel())
+        assert rel(got[x].ravel(), ref) < OP_TOL, x
+
+
+def test_batched_slice_recon_matches_per_slice_oracle(cuda):
+    """Config-2 style: S independent slices (own PCA compression, shared ky-kz mask) in one
+    batched engine run, each against the oracle's per-slice Algorithm 1."""
+    cs, fm, lo, sk, so = _api()
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.parallel_recon import compress_slices
+    from paper_2305_06482_b200.plan import cartesian_plan
+    rng = np.random.default_rng(9)
+    S, C, dims = 3, 8, (32, 40)
+    mask = synth.vd_poisson_mask(dims, 3.0, 8, 5)
+    pts = synth.mask_points(mask)
+    maps = np.stack([synth.gaussian_coil_maps(dims, C, rng) for _ in range(S)])
+    imgs = np.stack([synth.random_ellipses(dims, 4, rng).ravel() for _ in range(S)])
+    okern = O.CartesianKernel(dims, pts)
+    data = np.stack([O.Sense(maps[s], okern).forward(imgs[s]).reshape(C, -1) for s in range(S)])
+    data = data + synth.complex_noise(data.shape, 0.01 * np.abs(data).max(), rng)
+    kern = CartesianKernel(dims, [cartesian_plan(dims, pts)], batch=S)
+    maps0, y0, comp = compress_slices(torch.from_numpy(maps.astype(np.complex64)).cuda(),
+                                      torch.from_numpy(data.astype(np.complex64)).cuda(), C)
+    reg = so.make_regularizer("l1-wavelet", 1e-3, lo.GridShape(dims))
+    cfg = cs.CoilSketchConfig(C, sk.SketchConfig(4, 2, 2, rademacher_scale=12 ** -0.5), reg, 3, 4)
+    res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
+    x = res.x.cpu().numpy()
+    for s in range(S):
+        ref = O.coil_sketching_recon(data[s], maps[s], dims, lambda: okern, c_hat0=C, v=2, s=2, lam=1e-3,
+                                     outer=3, inner=4, rademacher_scale=12 ** -0.5)
+        nrmse = np.linalg.norm(np.abs(x[s]) - np.abs(ref.x_final)) / np.linalg.norm(ref.x_final)
+        assert nrmse <= IMG_TOL, (s, nrmse)
+        np.testing.assert_allclose(res.objectives[:, s], ref.objectives, rtol=1e-4)
