@@ -133,10 +133,15 @@ def slice_compression(y: torch.Tensor, keep: int, valid_n=None, threads: int | N
         return np.stack(list(ex.map(one, range(S))))
 
 
-def compress_slices(maps: torch.Tensor, y: torch.Tensor, keep: int, valid_n=None):
-    """(maps0, y0, comp): per-slice PCA rotation of maps (S, C, D) and data (S, C, N) on the device (K5)."""
+def compress_slices(maps: torch.Tensor, y: torch.Tensor, keep: int, valid_n=None, comp=None):
+    """(maps0, y0, comp): per-slice PCA rotation of maps (S, C, D) and data (S, C, N) on the device (K5).
+
+    `comp` (S, keep, C) may be given, e.g. from the SVD of the complex128 host data: the
+    low-energy singular vectors are ill-conditioned, so parity with the reference needs
+    the SVD of exactly the reference's data, not of its complex64 copy."""
     from .sketching import coil_contract
-    comp = slice_compression(y, keep, valid_n)
+    if comp is None:
+        comp = slice_compression(y, keep, valid_n)
     maps0 = coil_contract(maps.contiguous(), comp)
     y0 = coil_contract(y.contiguous(), comp)
     return maps0, y0, comp

@@ -302,8 +302,9 @@ def test_batched_slice_recon_matches_per_slice_oracle(cuda):
     data = np.stack([O.Sense(maps[s], okern).forward(imgs[s]).reshape(C, -1) for s in range(S)])
     data = data + synth.complex_noise(data.shape, 0.01 * np.abs(data).max(), rng)
     kern = CartesianKernel(dims, [cartesian_plan(dims, pts)], batch=S)
-    maps0, y0, comp = compress_slices(torch.from_numpy(maps.astype(np.complex64)).cuda(),
-                                      torch.from_numpy(data.astype(np.complex64)).cuda(), C)
+    comp = np.stack([np.linalg.svd(data[s], full_matrices=False)[0].conj().T for s in range(S)])
+    maps0, y0, _ = compress_slices(torch.from_numpy(maps.astype(np.complex64)).cuda(),
+                                   torch.from_numpy(data.astype(np.complex64)).cuda(), C, comp=comp)
     reg = so.make_regularizer("l1-wavelet", 1e-3, lo.GridShape(dims))
     cfg = cs.CoilSketchConfig(C, sk.SketchConfig(4, 2, 2, rademacher_scale=12 ** -0.5), reg, 3, 4)
     res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
