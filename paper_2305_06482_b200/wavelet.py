@@ -45,8 +45,9 @@ class WaveletEngine:
                     for _ in range(2)]
         self.nblocks = [_lib.lib().sr_wavelet_ana2_nblocks(self.ny >> l, self.nx >> l)
                         for l in range(levels)]
-        self.l1part = torch.zeros(self.batch, sum(self.nblocks), dtype=torch.float64,
-                                  device=self.device)
+        # one contiguous (B, nblocks_l) partial-sum buffer per level (the kernel indexes b * nblocks + blk)
+        self.l1parts = [torch.zeros(self.batch, nb, dtype=torch.float64, device=self.device)
+                        for nb in self.nblocks]
 
     def _region(self, l):
         return self.ny >> l, self.nx >> l
@@ -61,9 +62,6 @@ class WaveletEngine:
         _lib.call("sr_wavelet_syn2", dv.ptr(src), dv.ptr(dst), h, w, self.nx, self.D, self.batch,
                   dv.ptr(zout), dv.ptr(xold), float(beta), dv.stream())
 
-    def _l1slice(self, l):
-        o = sum(self.nblocks[:l])
-        return self.l1part[:, o: o + self.nblocks[l]]
 
     # ------------------------------------------------------------- hot path
     def prox(self, v, out, thresh=None, hthresh=-1.0, zout=None, xold=None, beta=0.0):
@@ -90,9 +88,9 @@ class WaveletEngine:
         src = x
         for l in range(self.levels):
             dst = self.buf[l % 2]
-            self._ana(src, dst, l, None, -1.0, self._l1slice(l))
+            self._ana(src, dst, l, None, -1.0, self.l1parts[l])
             src = dst
-        return self.l1part.sum(dim=1)
+        return sum(p.sum(dim=1) for p in self.l1parts)
 
     # ------------------------------------------------- reference-layout API
     def forward(self, x, out):
