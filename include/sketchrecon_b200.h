@@ -119,6 +119,16 @@ int sr_wavelet_ana2_nblocks(int h, int w);
 int sr_wavelet_syn2(const sr_c64* coef, sr_c64* out, int h, int w, int ld, long long bs,
                     int batch, sr_c64* zout, const sr_c64* xold, float beta, void* stream);
 int sr_wavelet_levels_max(void);
+/* K6 n-D -- one axis of one DB4 level (analysis or synthesis) over the (h0, h1, h2)
+ * corner of (n0, n1, n2) arrays, for 1-D and 3-D grids (linops.py:619-651, 677-702);
+ * thr_enable (analysis, last axis of a level) soft-thresholds the detail sub-bands
+ * (and the low-pass corner when last_level) and fills l1part (batch, nblocks);
+ * zout/xold/beta: FISTA momentum epilogue on the final synthesis launch. */
+int sr_wavelet_axis(const sr_c64* src, sr_c64* dst, int h0, int h1, int h2, int n1, int n2, long long bs,
+                    int batch, int axis, int inverse, const float* thresh, float hthresh, int thr_enable,
+                    int last_level, double* l1part, sr_c64* zout, const sr_c64* xold, float beta,
+                    void* stream);
+int sr_wavelet_axis_nblocks(void);
 
 /* K7 -- deterministic per-slice reductions (fixed-order, no atomics).
  * mode 0: sum |a|^2   1: sum conj(a) b   2: sum |a|   3: sum |a - b|^2

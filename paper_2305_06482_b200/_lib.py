@@ -30,6 +30,8 @@ SIGNATURES = {
     "sr_wavelet_ana2_nblocks": [_i, _i],
     "sr_wavelet_syn2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _vp, _f, _vp],
     "sr_wavelet_levels_max": [],
+    "sr_wavelet_axis": [_vp, _vp, _i, _i, _i, _i, _i, _ll, _i, _i, _i, _vp, _f, _i, _i, _vp, _vp, _vp, _f, _vp],
+    "sr_wavelet_axis_nblocks": [],
     "sr_reduce": [_i, _vp, _vp, _ll, _ll, _i, _vp, _vp, _vp],
     "sr_reduce_nparts": [],
     "sr_lincomb": [_vp, _vp, _vp, _vp, _vp, _f, _f, _f, _ll, _ll, _i, _vp],

@@ -1,0 +1,156 @@
+// K6 (n-D): one axis of one level of the periodic DB4 wavelet, for 1-D and 3-D
+// grids (2-D grids use the tiled kernels of wavelet.cu).  BASELINE config 4
+// reconstructs a 256 x 256 x 160 volume, so its L1-wavelet prox is 3-D.
+//
+// Reference: _analysis_axis / _synthesis_axis (linops.py:619-651); WaveletOp
+// applies the analysis along axes 0..d-1 on the low-pass corner of each level
+// and the synthesis in reverse axis order (linops.py:677-702).  Each launch
+// here is one axis over the (h0, h1, h2) corner of arrays shaped (n0, n1, n2)
+// (leading 1s for lower dimensions); src and dst never alias.  The last axis of
+// a level may apply the soft threshold to the detail sub-bands (and to the
+// low-pass corner at the coarsest level) and collect sum |c| partials; the last
+// synthesis launch may apply the FISTA momentum epilogue.
+#include "common.cuh"
+
+namespace {
+
+__constant__ float c_lo[8] = {
+    -0.010597401785069032105f, 0.032883011666885199735f, 0.030841381835560763627f,
+    -0.18703481171909308408f, -0.027983769416859854211f, 0.63088076792985890788f,
+    0.71484657055291564709f, 0.23037781330889650086f};
+__constant__ float c_hi[8] = {
+    0.23037781330889650086f, -0.71484657055291564709f, 0.63088076792985890788f,
+    0.027983769416859854211f, -0.18703481171909308408f, -0.030841381835560763627f,
+    0.032883011666885199735f, 0.010597401785069032105f};
+
+struct AxisArgs {
+  const float2* src;
+  float2* dst;
+  int h[3];         // region extent
+  long long st[3];  // element strides of the full array
+  long long bs;     // slice stride
+  int axis;
+  int inverse;
+  const float* thresh;  // per-slice thresholds (device) or null
+  float hthresh;        // host threshold (< 0: none)
+  int thr_enable;       // apply threshold (last axis of an analysis level)
+  int last_level;       // threshold the low-pass corner too
+  double* l1part;       // (batch, gridDim.x) partial sums or null
+  float2* zout;         // synthesis epilogue z = v + beta (v - xold)
+  const float2* xold;
+  float beta;
+};
+
+__global__ void __launch_bounds__(256) k_wav_axis(AxisArgs a) {
+  const int b = blockIdx.y;
+  const long long total = (long long)a.h[0] * a.h[1] * a.h[2];
+  const int ax = a.axis;
+  const int n = a.h[ax], hn = n >> 1;
+  const long long sa = a.st[ax];
+  const float2* src = a.src + b * a.bs;
+  float2* dst = a.dst + b * a.bs;
+  double part = 0.0;
+  const float t = a.thresh ? a.thresh[b] : a.hthresh;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i2 = (int)(e % a.h[2]);
+    const long long q = e / a.h[2];
+    const int i1 = (int)(q % a.h[1]);
+    const int i0 = (int)(q / a.h[1]);
+    const int ii[3] = {i0, i1, i2};
+    const long long off = i0 * a.st[0] + i1 * a.st[1] + i2 * a.st[2];
+    const long long line = off - (long long)ii[ax] * sa;  // start of this line along `ax`
+    const int m = ii[ax];
+    float2 v = make_float2(0.f, 0.f);
+    if (!a.inverse) {
+      const bool is_hi = m >= hn;
+      const int i = is_hi ? m - hn : m;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float f = is_hi ? c_hi[k] : c_lo[k];
+        const float2 x = src[line + (long long)((2 * i + k) % n) * sa];
+        v.x = fmaf(f, x.x, v.x);
+        v.y = fmaf(f, x.y, v.y);
+      }
+      if (a.thr_enable) {
+        bool lowpass = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          if (a.h[d] > 1 && ii[d] >= (a.h[d] >> 1)) lowpass = false;
+        const bool final_coef = !lowpass || a.last_level;
+        if (final_coef && (a.thresh || a.hthresh >= 0.f)) {
+          const float mg = sqrtf(v.x * v.x + v.y * v.y);
+          const float s = (mg > t) ? (mg - t) / mg : 0.f;
+          v = make_float2(v.x * s, v.y * s);
+        }
+        if (final_coef && a.l1part) part += sqrt((double)v.x * v.x + (double)v.y * v.y);
+      }
+    } else {
+      const int par = m & 1;
+#pragma unroll
+      for (int tt = 0; tt < 4; ++tt) {
+        const int k = par + 2 * tt;
+        int i = ((m - k) / 2) % hn;
+        if (i < 0) i += hn;
+        const float2 lo = src[line + (long long)i * sa];
+        const float2 hi = src[line + (long long)(hn + i) * sa];
+        v.x = fmaf(c_lo[k], lo.x, fmaf(c_hi[k], hi.x, v.x));
+        v.y = fmaf(c_lo[k], lo.y, fmaf(c_hi[k], hi.y, v.y));
+      }
+      if (a.zout) {
+        const float2 xo = a.xold[b * a.bs + off];
+        a.zout[b * a.bs + off] = make_float2(fmaf(a.beta, v.x - xo.x, v.x), fmaf(a.beta, v.y - xo.y, v.y));
+      }
+    }
+    dst[off] = v;
+  }
+  if (a.l1part) {
+    __shared__ double red[256];
+    red[threadIdx.x] = part;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.l1part[(long long)b * gridDim.x + blockIdx.x] = red[0];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sr_wavelet_axis_nblocks(void) { return 148 * 4; }
+
+// One axis of one level over the (h0, h1, h2) corner of (n0, n1, n2) arrays.
+int sr_wavelet_axis(const sr_c64* src, sr_c64* dst, int h0, int h1, int h2, int n1, int n2, long long bs,
+                    int batch, int axis, int inverse, const float* thresh, float hthresh, int thr_enable,
+                    int last_level, double* l1part, sr_c64* zout, const sr_c64* xold, float beta,
+                    void* stream) {
+  if (batch < 1 || axis < 0 || axis > 2 || h0 < 1 || h1 < 1 || h2 < 1) return SR_EINVAL;
+  const int h[3] = {h0, h1, h2};
+  if (h[axis] < 2 || (h[axis] & 1)) return SR_EINVAL;
+  if ((const void*)src == (const void*)dst) return SR_EINVAL;
+  AxisArgs a;
+  a.src = (const float2*)src;
+  a.dst = (float2*)dst;
+  a.h[0] = h0; a.h[1] = h1; a.h[2] = h2;
+  a.st[0] = (long long)n1 * n2; a.st[1] = n2; a.st[2] = 1;
+  a.bs = bs;
+  a.axis = axis;
+  a.inverse = inverse;
+  a.thresh = thresh;
+  a.hthresh = hthresh;
+  a.thr_enable = thr_enable;
+  a.last_level = last_level;
+  a.l1part = l1part;
+  a.zout = (float2*)zout;
+  a.xold = (const float2*)xold;
+  a.beta = beta;
+  dim3 grid(sr_wavelet_axis_nblocks(), batch);
+  k_wav_axis<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
+}  // extern "C"

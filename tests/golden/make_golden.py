@@ -221,6 +221,57 @@ def main():
     recon_case("recon_radial", (16, 16), 4, 4, 2, 1, 5e-4, 2, 3, 1.0 / np.sqrt(12),
                nufft=(16, 32, 2.0, 4))
 
+    # --- 1-D / 3-D wavelets (appended: earlier fixtures keep their RNG stream)
+    for name, dims in [("wavelet_3d", (16, 12, 8)), ("wavelet_1d", (64,))]:
+        shape = lo.GridShape(dims)
+        w = lo.WaveletOp(shape)
+        xx = crandn(g, shape.size)
+        reg = so.make_regularizer("l1-wavelet", 0.3, shape)
+        out[name] = dict(dims=np.array(dims), levels=np.array(w.levels), x=xx, fwd=w.forward(xx),
+                         adj=w.adjoint(xx), prox=reg.prox(xx, 0.7), value=np.array(reg.value(xx)))
+    # --- 3-D non-Cartesian (config-4 style, reduced) end to end
+    recon_case_3d = dict(dims=(16, 16, 12), C=4, chat0=4, v=2, s=2, lam=1e-3, T=2, K=3)
+    dims = recon_case_3d["dims"]
+    shape = lo.GridShape(dims)
+    C = recon_case_3d["C"]
+    maps = smooth_maps(g, dims, C)
+    grids = np.meshgrid(*[np.linspace(-1, 1, n, endpoint=False) for n in dims], indexing="ij")
+    img = np.zeros(dims, complex)
+    for _ in range(3):
+        c = g.uniform(-0.3, 0.3, 3); ax = g.uniform(0.2, 0.5, 3)
+        img += g.uniform(0.2, 1.0) * (sum(((gg - cc) / aa) ** 2 for gg, cc, aa in zip(grids, c, ax)) <= 1)
+    # cones-like: random points on shells, kept inside [-n/2, n/2)
+    npts = 1500
+    rad = g.uniform(0, 1, npts) ** 0.7
+    th = np.arccos(g.uniform(-1, 1, npts)); ph = g.uniform(0, 2 * np.pi, npts)
+    half = np.array(dims) / 2 * 0.999
+    pts = np.stack([rad * np.cos(th), rad * np.sin(th) * np.cos(ph), rad * np.sin(th) * np.sin(ph)], 1) * half
+    traj = lo.Trajectory(pts, "non-cartesian")
+    weights = fm.radial_density_weights(traj)
+    kern = lo._GriddedNUFFTKernel(shape, traj, 1.25, 4)
+    a = fm.SenseOperator(fm.SensitivityMaps(shape, maps), traj, kernel=kern)
+    clean = a.forward_unweighted(img.ravel()).reshape(C, -1)
+    data = clean + (g.standard_normal(clean.shape) + 1j * g.standard_normal(clean.shape)) * 0.01 * np.abs(clean).max() / np.sqrt(2)
+    orig_gen, orig_mk = cs.gen_sketch_matrix, fm.make_fourier_kernel
+    cs.gen_sketch_matrix = scaled_gen(sk, 1.0 / np.sqrt(12))
+    fm.make_fourier_kernel = lambda sh, tr, method="auto": lo._GriddedNUFFTKernel(sh, tr, 1.25, 4)
+    try:
+        reg = so.make_regularizer("l1-wavelet", 1e-3, shape)
+        cfg = cs.CoilSketchConfig(4, sk.SketchConfig(4, 2, 2, "rademacher", 0), reg, 2, 3)
+        rep = cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps), cfg,
+                                      weights=weights)
+    finally:
+        cs.gen_sketch_matrix, fm.make_fourier_kernel = orig_gen, orig_mk
+    out["recon_cones3d"] = dict(dims=np.array(dims), points=pts, maps=maps, data=data, truth=img.ravel(),
+                                chat0=np.array(4), v=np.array(2), s=np.array(2), lam=np.array(1e-3),
+                                outer=np.array(2), inner=np.array(3), scale=np.array(1.0 / np.sqrt(12)),
+                                x_final=rep.x_final.values,
+                                objectives=np.array([r.objective for r in rep.per_outer]),
+                                counts=np.array(rep.counts.get("coil_transform", 0)),
+                                expected=np.array(cs.expected_coil_transforms(cfg, so.SolverConfig(tol=0.0))),
+                                diverged=np.array(rep.diverged), weights=weights.w,
+                                oversamp=np.array(1.25), width=np.array(4))
+
     for k, v in out.items():
         np.savez_compressed(OUT / f"{k}.npz", **v)
     print("wrote", ", ".join(sorted(out)))

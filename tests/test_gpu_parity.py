@@ -66,7 +66,7 @@ def test_kernel_plugin_protocol(cuda):
     assert rel(a.normal(g["x"]), g["AHAx"]) < OP_TOL
 
 
-@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24"])
+@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24", "wavelet_3d", "wavelet_1d"])
 def test_wavelet_and_prox(cuda, name):
     cs, fm, lo, sk, so = _api()
     g = golden(name)
@@ -245,8 +245,9 @@ def test_nufft_large_2d_vs_oracle(cuda):
     assert rel(y.cpu().numpy().ravel(), O.Sense(maps, ok, w).forward(x)) < OP_TOL
 
 
-def test_coil_sketching_recon_radial_matches_reference(cuda):
-    g = golden("recon_radial")
+@pytest.mark.parametrize("name", ["recon_radial", "recon_cones3d"])
+def test_coil_sketching_recon_noncartesian_matches_reference(cuda, name):
+    g = golden(name)
     cs, fm, lo, sk, so, dims, shape, traj, nufft = _recon_inputs(g)
     from paper_2305_06482_b200.nufft import GriddedKernel
     reg = so.make_regularizer("l1-wavelet", float(g["lam"]), shape)

@@ -55,7 +55,7 @@ def test_cartesian_sense(name):
     assert abs(lam - float(g["lam_max"])) < 1e-10 * abs(float(g["lam_max"]))
 
 
-@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24"])
+@pytest.mark.parametrize("name", ["wavelet_32x32", "wavelet_40x16", "wavelet_20x24", "wavelet_3d", "wavelet_1d"])
 def test_wavelet(name):
     g = golden(name)
     dims = tuple(g["dims"])
@@ -100,7 +100,8 @@ def _kernel_for(g):
 @pytest.mark.parametrize("name,solver,reg", [("recon_cart", "fista", "l1-wavelet"),
                                              ("recon_cart_pm1", "fista", "l1-wavelet"),
                                              ("recon_cart_cg", "cg", "l2"),
-                                             ("recon_radial", "fista", "l1-wavelet")])
+                                             ("recon_radial", "fista", "l1-wavelet"),
+                                             ("recon_cones3d", "fista", "l1-wavelet")])
 def test_recon_end_to_end(name, solver, reg):
     g = golden(name)
     dims = tuple(g["dims"])
