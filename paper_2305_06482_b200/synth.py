@@ -129,3 +129,40 @@ def golden_angle_radial(n_spokes: int, n_read: int, dims) -> np.ndarray:
 def complex_noise(shape, sigma: float, rng: np.random.Generator) -> np.ndarray:
     """Complex Gaussian noise, std sigma/sqrt(2) per component (simulate.py:347-352)."""
     return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) * (sigma / math.sqrt(2.0))
+
+
+def cones_3d(dims, n_cones: int = 32, n_readouts: int = 18000, n_samples: int = 512,
+             turns: float = 4.0, seed: int = 0) -> np.ndarray:
+    """3-D conical-spiral trajectory (BASELINE config 4), cycles/FOV per axis.
+
+    `n_cones` polar angles uniform in (0, pi/2], mirrored to both hemispheres;
+    interleaves per cone proportional to sin(theta) (about `n_readouts` in total);
+    each readout a conical spiral of `n_samples` samples whose radius grows
+    linearly to k_max = pi rad.  The cone axis is the last image axis.  k is
+    scaled by (1 - 1e-6) so every coordinate lies in [-n/2, n/2) as
+    Trajectory.validate_for requires (linops.py:130-140).
+    """
+    rng = np.random.default_rng(seed)
+    th = np.arange(1, n_cones + 1) * (np.pi / 2) / n_cones
+    weights = np.sin(th)
+    per = np.maximum(1, np.round(weights / weights.sum() * (n_readouts / 2))).astype(int)
+    t = np.arange(n_samples) / n_samples  # radius fraction in [0, 1)
+    out = []
+    for theta, n_il in zip(th, per):
+        for sign in (1.0, -1.0):
+            phi0 = rng.uniform(0, 2 * np.pi) + 2 * np.pi * np.arange(n_il)[:, None] / n_il
+            phi = phi0 + 2 * np.pi * turns * t[None, :]
+            r = np.pi * t[None, :]
+            kz = sign * r * np.cos(theta)
+            kx = r * np.sin(theta) * np.cos(phi)
+            ky = r * np.sin(theta) * np.sin(phi)
+            out.append(np.stack([kx.ravel(), ky.ravel(), np.broadcast_to(kz, kx.shape).ravel()], axis=1))
+    k = np.concatenate(out, axis=0) * (1 - 1e-6)
+    n = np.asarray(dims, dtype=np.float64)
+    return k * n / (2 * np.pi)
+
+
+def coil_maps_cylinder(dims, n_coils: int, rng: np.random.Generator, radius: float = 1.5, sigma: float = 0.6,
+                       xp=np, device=None):
+    """3-D Gaussian coils on a cylinder around the last axis (BASELINE configs 2, 4)."""
+    return gaussian_coil_maps(dims, n_coils, rng, radius=radius, sigma=sigma, xp=xp, device=device)
