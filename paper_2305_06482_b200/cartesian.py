@@ -108,6 +108,58 @@ class CartesianKernel:
                   ncoils, self.ny, self.nx, dv.ptr(coef), dv.ptr(u), dv.ptr(d), chunk, dv.stream())
         return out
 
+    def _normal_range(self, maps, x, out, b0: int, b1: int, ws, stream: int):
+        """K1 over slices [b0, b1) of the batch (device pointers offset, three-launch schedule)."""
+        ncoils, mbs = self._maps_stride(maps)
+        item = 8  # bytes per complex64
+        xo = b0 * self.D * item
+        _lib.call("sr_cart_normal", dv.ptr(x) + xo, None, dv.ptr(maps) + b0 * mbs * item, mbs,
+                  dv.ptr(self.maskT) + b0 * self.mask_bstride, self.mask_bstride, dv.ptr(out) + xo,
+                  dv.ptr(ws), b1 - b0, ncoils, self.ny, self.nx, None, None, None, 0, stream)
+
+    def normal_host(self, maps, x_host, out_host, *, chunks: int = 8, buffers=None):
+        """A^H A on HOST (pinned) buffers, pipelined: slice chunks are copied in, applied and
+        copied out on three streams so PCIe transfers overlap the K1 launches.
+
+        x_host/out_host: pinned (B, D) complex64 CPU tensors.  Returns out_host (synchronised).
+        `buffers` = (x_dev, out_dev) device staging tensors to reuse across calls.
+        """
+        import torch
+        if x_host.device.type != "cpu" or out_host.device.type != "cpu":
+            raise ValueError("normal_host takes host tensors")
+        ncoils, _ = self._maps_stride(maps)
+        B = self.batch
+        chunks = max(1, min(int(chunks), B))
+        bounds = [(B * i // chunks, B * (i + 1) // chunks) for i in range(chunks)]
+        if buffers is None:
+            buffers = (torch.empty(B, self.D, dtype=torch.complex64, device=self.device),
+                       torch.empty(B, self.D, dtype=torch.complex64, device=self.device))
+        xd, od = buffers
+        ws = self.workspace(ncoils, batch=max(b1 - b0 for b0, b1 in bounds), chunk=0)
+        cur = torch.cuda.current_stream()
+        if not hasattr(self, "_streams"):
+            self._streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        s_in, s_out = self._streams
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        done_in = []
+        for b0, b1 in bounds:
+            with torch.cuda.stream(s_in):
+                xd[b0:b1].copy_(x_host[b0:b1], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+                done_in.append(e)
+        for (b0, b1), e in zip(bounds, done_in):
+            cur.wait_event(e)
+            self._normal_range(maps, xd, od, b0, b1, ws, cur.cuda_stream)
+            ec = torch.cuda.Event()
+            ec.record(cur)
+            s_out.wait_event(ec)
+            with torch.cuda.stream(s_out):
+                out_host[b0:b1].copy_(od[b0:b1], non_blocking=True)
+        cur.wait_stream(s_out)
+        return out_host
+
     def partial_shape(self, ncoils: int) -> tuple:
         """Shape of the residual partial-sum buffer `forward(partial=...)` fills."""
         return (self.batch, ncoils, 64)

@@ -316,3 +316,20 @@ def test_batched_slice_recon_matches_per_slice_oracle(cuda):
         nrmse = np.linalg.norm(np.abs(x[s]) - np.abs(ref.x_final)) / np.linalg.norm(ref.x_final)
         assert nrmse <= IMG_TOL, (s, nrmse)
         np.testing.assert_allclose(res.objectives[:, s], ref.objectives, rtol=1e-4)
+
+
+def test_normal_host_pipelined_matches_device(cuda):
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    rng = np.random.default_rng(12)
+    dims, B, C = (64, 40), 5, 3
+    plans = [cartesian_plan(dims, np.argwhere(rng.random(dims) < 0.3) - np.array([32, 20])) for _ in range(B)]
+    kern = CartesianKernel(dims, plans)
+    D = dims[0] * dims[1]
+    maps = torch.from_numpy((rng.standard_normal((B, C, D)) + 1j * rng.standard_normal((B, C, D))).astype(np.complex64)).cuda()
+    x = torch.from_numpy((rng.standard_normal((B, D)) + 1j * rng.standard_normal((B, D))).astype(np.complex64))
+    ref = torch.empty(B, D, dtype=torch.complex64, device="cuda")
+    kern.normal(maps, x.cuda(), ref)
+    out = torch.empty(B, D, dtype=torch.complex64).pin_memory()
+    kern.normal_host(maps, x.pin_memory(), out, chunks=3)
+    assert rel(out.numpy(), ref.cpu().numpy()) < 1e-6
