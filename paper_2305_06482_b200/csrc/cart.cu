@@ -46,7 +46,7 @@ struct RowCfg {
   static constexpr int XS = N + ((((P % 16) - (N % 16)) % 16 + 16) % 16);  // x row stride = P (mod 16)
   // dynamic smem (float2): twiddles N | work rows ROWS*VS | [fwd only] staged x ROWS*XS
   static constexpr size_t SMEM_FWD = sizeof(float2) * (N + ROWS * FftShape<P, Q>::VS + ROWS * XS);
-  static constexpr size_t SMEM_INV = sizeof(float2) * (N + ROWS * FftShape<P, Q>::VS);
+  static constexpr size_t SMEM_INV = sizeof(float2) * (N + 2 * ROWS * FftShape<P, Q>::VS);
 };
 
 template <int P, int Q>
@@ -88,11 +88,19 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   const float2* xr = xs + lr * XS + p;
+  // software pipeline: coil j+1's map values are loaded while coil j is transformed
+  float2 mcur[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) mcur[q] = valid ? __ldg(mb + P * q) : make_float2(0.f, 0.f);
   for (int j = 0; j < ncoils; ++j) {
     float2 r[Q];
-    const float2* mr = mb + j * D;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) r[q] = valid ? cmul(__ldg(mr + P * q), xr[P * q]) : make_float2(0.f, 0.f);
+    for (int q = 0; q < Q; ++q) r[q] = cmul(mcur[q], xr[P * q]);
+    if (j + 1 < ncoils && valid) {
+      const float2* mn = mb + (j + 1) * D;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) mcur[q] = __ldg(mn + P * q);
+    }
     fft_s1_fwd<P, Q>(r, p, t1);
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
@@ -132,7 +140,7 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   extern __shared__ __align__(16) float2 dsm[];
   float2* t2 = dsm;
-  float2* buf = dsm + N;
+  float2* bufs = dsm + N;  // two tiles of ROWS * VS (double buffer)
   const int tid = threadIdx.x;
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
@@ -147,13 +155,31 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   const float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   const int nvalid = min(ROWS, ny - row0) * N;
-  for (int j = 0; j < ncoils; ++j) {
+  auto issue_tile = [&](int j) {
     const float2* wj = wb + j * D;
+    float2* dst = bufs + (j & 1) * (ROWS * S::VS);
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
-      buf[l3 * S::VS + S::pad(pos)] = wj[e];
+      cp_async8(dst + l3 * S::VS + S::pad(pos), wj + e);
+    }
+    cp_async_commit();
+  };
+  issue_tile(0);
+  for (int j = 0; j < ncoils; ++j) {
+    if (j + 1 < ncoils) {
+      issue_tile(j + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    float2* buf = bufs + (j & 1) * (ROWS * S::VS);
+    float2 mreg[Q];
+    {
+      const float2* mr = mb + j * D;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) mreg[q] = valid ? __ldg(mr + P * q) : make_float2(0.f, 0.f);
+    }
     if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
         const int l2 = it / Q, k2 = it - l2 * Q;
@@ -171,12 +197,9 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[lr * S::VS + S::GS * k2 + p];
     fft_s1_inv<Q>(r);
-    if (valid) {
-      const float2* mr = mb + j * D;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) cfma_conj(acc[q], __ldg(mr + P * q), r[q]);
-    }
-    __syncthreads();
+    for (int q = 0; q < Q; ++q) cfma_conj(acc[q], mreg[q], r[q]);
+    __syncthreads();  // buf (j & 1) is refilled by the prefetch issued next iteration
   }
   if (!valid) return;
   const long long off = b * x_bstride + (long long)row * N + p;

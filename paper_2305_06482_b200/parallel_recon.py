@@ -129,8 +129,18 @@ def slice_compression(y: torch.Tensor, keep: int, valid_n=None, threads: int | N
         u, _, _ = np.linalg.svd(yh[s, :, :n], full_matrices=False)
         return u[:, :keep].conj().T
 
-    with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, os.cpu_count() or 1))) as ex:
-        return np.stack(list(ex.map(one, range(S))))
+    try:  # one BLAS thread per SVD, parallel over slices
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(1)
+    except Exception:  # pragma: no cover
+        limit = None
+    try:
+        ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, ncpu))) as ex:
+            return np.stack(list(ex.map(one, range(S))))
+    finally:
+        if limit is not None:
+            limit.restore_original_limits()
 
 
 def compress_slices(maps: torch.Tensor, y: torch.Tensor, keep: int, valid_n=None, comp=None):

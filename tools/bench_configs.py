@@ -161,7 +161,11 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256):
     torch.cuda.synchronize()
     t_start = time.perf_counter()
     y = dec(kx.contiguous()) if dec is not None else y2
+    torch.cuda.synchronize()
+    t_dec = time.perf_counter()
     maps0, y0, comp = compress_slices(maps, y, C)
+    torch.cuda.synchronize()
+    t_comp = time.perf_counter()
     reg = so.make_regularizer("l1-wavelet", 1e-3, lo.GridShape(dims))
     cfg = cs.CoilSketchConfig(C, sk.SketchConfig(V + S, V, S, rademacher_scale=12 ** -0.5), reg, 10, 10)
     t_solve0 = time.perf_counter()
@@ -176,6 +180,7 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256):
         line = {"config": 2, "what": f"{nslices_total} readout-decoupled slices {dims}, C={C} -> {V}+{S}, 10x10 FISTA",
                 "n_gpus": world, "scaling": "strong", "gpu_wall_s": t_wall, "gpu_solve_s": t_solve,
                 "slices_per_s": nslices_total / t_wall, "k_decoupled_with_K8": dec is not None,
+                "readout_idft_s": t_dec - t_start, "compression_s": t_comp - t_dec,
                 "samples_per_slice": N, "data": "synthetic"}
     if with_oracle and rank == 0:
         # oracle on a bounded sample: the first 2 slices of rank 0 (same comp)
