@@ -32,6 +32,47 @@ namespace {
 // ------------------------------------------------------------------- pass A
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 
+// Row-tile layout of the row passes: groups of P padded by 2 (P even) so every
+// group starts 16-byte aligned -> the step-2 group moves and the tile copies are
+// 128-bit (LDS/STS/LDG/STG.128, cp.async 16 B).  Group stride GS/2 is odd in
+// 16-byte units, so the 8-lane phases of the 128-bit step-2 accesses are
+// conflict-free; VS = P (mod 16) keeps the 64-bit step-1 stores conflict-free.
+template <int P_, int Q_>
+struct RowShape {
+  static constexpr int P = P_, Q = Q_, N = P_ * Q_;
+  static constexpr bool VEC = (P_ % 2 == 0) && (P_ > 1);
+  static constexpr int GS = VEC ? P_ + 2 : (P_ == 1 ? 1 : P_ + 1);
+  static constexpr int VS0 = Q_ * GS;
+  static constexpr int VS = VS0 + ((((P_ % 16) - (VS0 % 16)) % 16 + 16) % 16);
+  __device__ __forceinline__ static int pad(int pos) { return (P_ == 1) ? pos : pos + (GS - P_) * (pos / P_); }
+};
+
+template <int P, bool VEC>
+__device__ __forceinline__ void lds_group(float2* g, const float2* gp) {
+  if constexpr (VEC) {
+#pragma unroll
+    for (int i = 0; i < P / 2; ++i) {
+      const float4 v = reinterpret_cast<const float4*>(gp)[i];
+      g[2 * i] = make_float2(v.x, v.y);
+      g[2 * i + 1] = make_float2(v.z, v.w);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) g[i] = gp[i];
+  }
+}
+template <int P, bool VEC>
+__device__ __forceinline__ void sts_group(float2* gp, const float2* g) {
+  if constexpr (VEC) {
+#pragma unroll
+    for (int i = 0; i < P / 2; ++i)
+      reinterpret_cast<float4*>(gp)[i] = make_float4(g[2 * i].x, g[2 * i].y, g[2 * i + 1].x, g[2 * i + 1].y);
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) gp[i] = g[i];
+  }
+}
+
 // ROWS rows per CTA, one thread per (row, p): T = ROWS * P is a whole number
 // of warps and at least 128 threads.
 template <int P, int Q>
@@ -40,13 +81,13 @@ struct RowCfg {
   static constexpr int ROWS0 = BASE * ((128 / (BASE * P)) > 1 ? (128 / (BASE * P)) : 1);
   static constexpr int ROWS = ROWS0 > 64 ? 64 : ROWS0;
   static constexpr int T = ROWS * P;
-  static constexpr int MINB = (T <= 160) ? 4 : 3;
+  static constexpr int MINB = (T <= 128) ? 4 : 3;
   static constexpr int MINB_INV = (T <= 128) ? 4 : 3;
   static constexpr int N = P * Q;
   static constexpr int XS = N + ((((P % 16) - (N % 16)) % 16 + 16) % 16);  // x row stride = P (mod 16)
   // dynamic smem (float2): twiddles N | work rows ROWS*VS | [fwd only] staged x ROWS*XS
-  static constexpr size_t SMEM_FWD = sizeof(float2) * (N + ROWS * FftShape<P, Q>::VS + ROWS * XS);
-  static constexpr size_t SMEM_INV = sizeof(float2) * (N + 2 * ROWS * FftShape<P, Q>::VS);
+  static constexpr size_t SMEM_FWD = sizeof(float2) * (N + ROWS * RowShape<P, Q>::VS + ROWS * XS);
+  static constexpr size_t SMEM_INV = sizeof(float2) * (N + 2 * ROWS * RowShape<P, Q>::VS);
 };
 
 template <int P, int Q>
@@ -54,7 +95,7 @@ __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          const float2* __restrict__ maps, float2* __restrict__ ws,
          int ncoils, int ny, long long x_bstride, long long map_bstride) {
-  using S = FftShape<P, Q>;
+  using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   constexpr int XS = RowCfg<P, Q>::XS;
   extern __shared__ __align__(16) float2 dsm[];
@@ -110,18 +151,23 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
         const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
         float2* gp = buf + l2 * S::VS + S::GS * k2;
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+        lds_group<P, S::VEC>(g, gp);
         fft_s2_fwd<P>(g);
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+        sts_group<P, S::VEC>(gp, g);
       }
       __syncthreads();
     }
     float2* wj = wb + j * D;
-    for (int e = tid; e < nvalid; e += T) {
-      const int l3 = e / N, pos = e - l3 * N;
-      wj[e] = buf[l3 * S::VS + S::pad(pos)];
+    if constexpr (S::VEC) {
+      for (int e = 2 * tid; e < nvalid; e += 2 * T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        *reinterpret_cast<float4*>(wj + e) = *reinterpret_cast<const float4*>(buf + l3 * S::VS + S::pad(pos));
+      }
+    } else {
+      for (int e = tid; e < nvalid; e += T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        wj[e] = buf[l3 * S::VS + S::pad(pos)];
+      }
     }
     __syncthreads();
   }
@@ -135,8 +181,8 @@ __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB_INV)
 k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
-         const float2* __restrict__ u, const float2* __restrict__ d) {
-  using S = FftShape<P, Q>;
+         const float2* __restrict__ u, const float2* __restrict__ d, float oscale) {
+  using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   extern __shared__ __align__(16) float2 dsm[];
   float2* t2 = dsm;
@@ -158,9 +204,16 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   auto issue_tile = [&](int j) {
     const float2* wj = wb + j * D;
     float2* dst = bufs + (j & 1) * (ROWS * S::VS);
-    for (int e = tid; e < nvalid; e += T) {
-      const int l3 = e / N, pos = e - l3 * N;
-      cp_async8(dst + l3 * S::VS + S::pad(pos), wj + e);
+    if constexpr (S::VEC) {
+      for (int e = 2 * tid; e < nvalid; e += 2 * T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        cp_async16(dst + l3 * S::VS + S::pad(pos), wj + e);
+      }
+    } else {
+      for (int e = tid; e < nvalid; e += T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        cp_async8(dst + l3 * S::VS + S::pad(pos), wj + e);
+      }
     }
     cp_async_commit();
   };
@@ -185,11 +238,9 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
         const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
         float2* gp = buf + l2 * S::VS + S::GS * k2;
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+        lds_group<P, S::VEC>(g, gp);
         fft_s2_inv<P, Q>(g, k2, t2);
-#pragma unroll
-        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+        sts_group<P, S::VEC>(gp, g);
       }
       __syncthreads();
     }
@@ -202,6 +253,8 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
     __syncthreads();  // buf (j & 1) is refilled by the prefetch issued next iteration
   }
   if (!valid) return;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = cscale(acc[q], oscale);  // 1/D of the unitary FFT pair
   const long long off = b * x_bstride + (long long)row * N + p;
   if (coef == nullptr) {
 #pragma unroll
@@ -286,8 +339,14 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
         for (int w4 = 0; w4 < P / 4; ++w4) {
           const uint32_t m4 = __ldg(reinterpret_cast<const uint32_t*>(mk) + w4);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            g[4 * w4 + i] = cscale(g[4 * w4 + i], ((m4 >> (8 * i)) & 0xffu) ? mscale : 0.f);
+          for (int i = 0; i < 4; ++i) {
+            const bool keep = (m4 >> (8 * i)) & 0xffu;
+            g[4 * w4 + i] = keep ? g[4 * w4 + i] : make_float2(0.f, 0.f);
+          }
+        }
+        if (mscale != 1.f) {
+#pragma unroll
+          for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mscale);
         }
       } else {
 #pragma unroll
@@ -394,7 +453,7 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
 template <int P, int Q>
 int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, int ncoils,
                   int ny, long long xbs, long long mbs, const float4* coef, const float2* u,
-                  const float2* d, cudaStream_t st) {
+                  const float2* d, float oscale, cudaStream_t st) {
   using R = RowCfg<P, Q>;
   static bool configured = false;
   if (!configured) {
@@ -404,7 +463,7 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
     configured = true;
   }
   dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
-  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d);
+  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d, oscale);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -441,12 +500,12 @@ int dispatch_rowfwd(int nx, const float2* x, const float2* anchor, const float2*
 
 int dispatch_rowinv(int nx, const float2* ws, const float2* maps, float2* out, int batch,
                     int ncoils, int ny, long long xbs, long long mbs, const float4* coef,
-                    const float2* u, const float2* d, cudaStream_t st) {
+                    const float2* u, const float2* d, float oscale, cudaStream_t st) {
   switch (nx) {
 #define X(N, P, Q)                                                                      \
   case N:                                                                               \
     return launch_rowinv<P, Q>(ws, maps, out, batch, ncoils, ny, xbs, mbs, coef, u, d, \
-                               st);
+                               oscale, st);
     SR_FFT_SIZES(X)
 #undef X
     default: return SR_EUNSUPPORTED;
@@ -529,10 +588,10 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
     const float2* dc = d ? (const float2*)d + xo : nullptr;
     int rc = dispatch_rowfwd(nx, xc, ac, mc, (float2*)ws, nb, ncoils, ny, D, map_bstride, st);
     if (rc) return rc;
-    rc = dispatch_colpass(ny, (float2*)ws, kc, mask_bstride, (float)(1.0 / (double)D), COL_NORMAL,
-                          nb, ncoils, nx, st);
+    rc = dispatch_colpass(ny, (float2*)ws, kc, mask_bstride, 1.f, COL_NORMAL, nb, ncoils, nx, st);
     if (rc) return rc;
-    rc = dispatch_rowinv(nx, (const float2*)ws, mc, oc, nb, ncoils, ny, D, map_bstride, cc, uc, dc, st);
+    rc = dispatch_rowinv(nx, (const float2*)ws, mc, oc, nb, ncoils, ny, D, map_bstride, cc, uc, dc,
+                         (float)(1.0 / (double)D), st);
     if (rc) return rc;
   }
   return SR_OK;
@@ -581,7 +640,7 @@ int sr_cart_adjoint(const sr_c64* y, long long ystride, const sr_c64* maps,
   if (rc) return rc;
   return dispatch_rowinv(nx, (const float2*)ws, (const float2*)maps, (float2*)out, batch,
                          ncoils, ny, D, map_bstride, (const float4*)coef, (const float2*)u,
-                         (const float2*)d, st);
+                         (const float2*)d, 1.f, st);
 }
 
 }  // extern "C"
