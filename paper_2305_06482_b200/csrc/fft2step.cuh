@@ -37,7 +37,7 @@ struct FftShape {
   __host__ __device__ __forceinline__ static int perm_pos(int k) { return P_ * (k % Q_) + k / Q_; }
 };
 
-// Twiddle tables, double-precision sincospi rounded once to float:
+// Twiddle tables (fp32 sincospif of an exactly reduced argument, |err| ~ 1 ulp):
 //   t1[k2*P + p] = W_N^{p k2}   (forward step 1; lanes vary p  -> conflict-free)
 //   t2[m1*Q + k2] = W_N^{m1 k2} (inverse step 2'; lanes vary k2 -> conflict-free)
 template <int P, int Q>
@@ -45,9 +45,9 @@ __device__ __forceinline__ void init_tw_s1(float2* t1, int tid, int nthreads) {
   constexpr int N = P * Q;
   for (int e = tid; e < N; e += nthreads) {
     const int k2 = e / P, p = e - k2 * P;
-    double s, c;
-    sincospi(-2.0 * (double)(p * k2) / (double)N, &s, &c);
-    t1[e] = make_float2((float)c, (float)s);
+    float s, c;
+    sincospif(-2.0f * (float)(p * k2) / (float)N, &s, &c);
+    t1[e] = make_float2(c, s);
   }
 }
 template <int P, int Q>
@@ -55,9 +55,9 @@ __device__ __forceinline__ void init_tw_s2(float2* t2, int tid, int nthreads) {
   constexpr int N = P * Q;
   for (int e = tid; e < N; e += nthreads) {
     const int m1 = e / Q, k2 = e - m1 * Q;
-    double s, c;
-    sincospi(-2.0 * (double)(m1 * k2) / (double)N, &s, &c);
-    t2[e] = make_float2((float)c, (float)s);
+    float s, c;
+    sincospif(-2.0f * (float)(m1 * k2) / (float)N, &s, &c);
+    t2[e] = make_float2(c, s);
   }
 }
 
