@@ -71,6 +71,9 @@ int sr_fused_normal_supported(int ny, int nx);
 /* Schedule of the fused K1 (process-wide): round r runs A(r), B(r - lagB), C(r - lagC);
  * `slots` slice slots of workspace ring (lagC < slots <= 8); tile = 8 or 16 rows/columns per item. */
 int sr_fused_config(int lagB, int lagC, int slots, int tile);
+/* Diagnostics of the fused K1: dev_buf = 8 device uint64 counters (spin iterations at the
+ * A-slot / B / C wait sites, then clock64 cycles spent in A / B / C items), NULL = off. */
+int sr_fused_stats(unsigned long long* dev_buf);
 
 /* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
  * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)

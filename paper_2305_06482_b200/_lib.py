@@ -40,6 +40,7 @@ SIGNATURES = {
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
     "sr_fused_normal_supported": [_i, _i],
     "sr_fused_config": [_i, _i, _i, _i],
+    "sr_fused_stats": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                         _vp, _vp, _vp, _vp],
     "sr_nufft_forward": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,

@@ -34,6 +34,21 @@ constexpr int MAX_SLOTS = 8;  // workspace ring capacity (runtime `slots` <= MAX
                               // lives in slot s % slots, stays in L2, and its dirty lines are
                               // overwritten before they would be evicted
 
+// optional wait statistics (sr_fused_stats): spin iterations per wait site, clock64 per item type
+__device__ unsigned long long* g_fused_stats = nullptr;
+
+__device__ __forceinline__ void spin_until(const int* c, int target, int site) {
+  unsigned long long n = 0;
+  int v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= target) break;
+    ++n;
+    __nanosleep(64);
+  }
+  if (g_fused_stats && n) atomicAdd(g_fused_stats + site, n);
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -73,15 +88,22 @@ __device__ __forceinline__ float2 ld_ro_hint(const float2* ptr, uint64_t pol) {
 
 template <int P, int QY, int QX, int TILE>
 struct FusedCfg {
-  using SX = FftShape<P, QX>;
-  using SY = FftShape<P, QY>;
+  using SX = RowShape<P, QX>;   // row tiles (A, C): 16-byte aligned groups
+  using SY = FftShape<P, QY>;   // column tiles (B): odd stride over columns
   static constexpr int NX = P * QX, NY = P * QY;
   static constexpr int T = TILE * P;
-  static constexpr int VSX = SX::VS;         // row-tile stride (= P mod 16)
-  static constexpr int VSPY = SY::VS0 | 1;   // column-tile stride (odd)
-  static constexpr int BUF = (TILE * VSX > TILE * VSPY) ? TILE * VSX : TILE * VSPY;
+  static constexpr int VSX = SX::VS;
+  static constexpr int VSPY = SY::VS0 | 1;
+  static constexpr int XS = NX + ((((P % 16) - (NX % 16)) % 16 + 16) % 16);  // staged x rows (A)
+  static constexpr int ROWT = TILE * VSX;
+  static constexpr int COLT = TILE * VSPY;
+  // buffer region: A = [row tile | x rows], B = [column tile], C = [row tile | row tile]
+  static constexpr int A_NEED = ROWT + TILE * XS, C_NEED = 2 * ROWT;
+  static constexpr int BUF0 = A_NEED > C_NEED ? A_NEED : C_NEED;
+  static constexpr int BUF1 = BUF0 > COLT ? BUF0 : COLT;
+  static constexpr int BUF = BUF1 + (BUF1 & 1);
   static constexpr int OFF_TX1 = 0, OFF_TX2 = NX, OFF_TY1 = 2 * NX, OFF_TY2 = 2 * NX + NY;
-  static constexpr int OFF_BUF = 2 * NX + 2 * NY;
+  static constexpr int OFF_BUF = 2 * NX + 2 * NY + ((2 * NX + 2 * NY) & 1);
   static constexpr size_t SMEM = sizeof(float2) * (OFF_BUF + BUF) + 16;  // + round table (ints)
 };
 
@@ -94,21 +116,26 @@ struct FusedArgs {
   long long mask_bstride;
   float2* out;
   float2* ws;     // ring of `slots` slice slots of (C, ny, nx), then the partial-sum ring
-  int* sync;      // [0] ticket, [1..] cntA[S*C], cntB[S*C], cntC[S]
+  int* sync;      // [0] ticket, [1..] cntA[S*C], cntB[S*C], cntC[S], cntT[S*nrt]
   int batch, ncoils;
   int lagB, lagC, slots;  // schedule: round r = {A(r), B(r - lagB), C(r - lagC)}
-  float mscale;
+  float oscale;           // 1/D of the unitary FFT pair, applied once per pixel
   const float4* coef;
   const float2* u;
   const float2* d;
 };
 
+constexpr int COILS_PER_A = 4;  // coils per A item (x staged once, maps prefetched one coil ahead)
+constexpr int COILS_PER_C = 3;  // coils per C item (partial coil sums, last arriver combines)
+
 // ---------------------------------------------------------------- A items
+// rows [rt*TILE, +TILE) of coils [j0, j1): u = c_j (x - a), row FFT -> workspace ring;
+// cntA[s, j] is released after every coil so B items of that coil can start early.
 template <int P, int QY, int QX, int TILE>
-__device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm) {
+__device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j0, int j1, float2* sm, int* cntA) {
   using F = FusedCfg<P, QY, QX, TILE>;
   using SX = typename F::SX;
-  constexpr int NX = F::NX, NY = F::NY, T = F::T;
+  constexpr int NX = F::NX, NY = F::NY, T = F::T, XS = F::XS;
   const int tid = threadIdx.x;
   const int lr = tid / P, p = tid - lr * P;
   const int row = rt * TILE + lr;
@@ -116,41 +143,57 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j, float2* sm
   const long long D = (long long)NX * NY;
   const float2* tx1 = sm + F::OFF_TX1;
   float2* buf = sm + F::OFF_BUF;
-  float2 r[QX];
+  float2* xs = buf + F::ROWT;
+  const int nrows = min(TILE, NY - rt * TILE);
+  const int nvalid = nrows * NX;
   {
-    const long long xo = (long long)s * D + (long long)row * NX + p;
-    const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
-#pragma unroll
-    for (int q = 0; q < QX; ++q) {
+    const float2* xb = a.x + (long long)s * D + (long long)rt * TILE * NX;
+    const float2* ab = a.anchor ? a.anchor + (long long)s * D + (long long)rt * TILE * NX : nullptr;
+    for (int e = tid; e < TILE * NX; e += T) {
+      const int l3 = e / NX, pos = e - l3 * NX;
       float2 v = make_float2(0.f, 0.f);
-      if (valid) {
-        v = __ldg(a.x + xo + P * q);
-        if (a.anchor) v = csub(v, __ldg(a.anchor + xo + P * q));
-        v = cmul(__ldg(mr + P * q), v);
+      if (e < nvalid) {
+        v = __ldg(xb + e);
+        if (ab) v = csub(v, __ldg(ab + e));
       }
-      r[q] = v;
+      xs[l3 * XS + pos] = v;
     }
   }
-  fft_s1_fwd<P, QX>(r, p, tx1);
+  const float2* mb = a.maps + s * a.map_bstride + (long long)row * NX + p;
+  float2 mcur[QX];
 #pragma unroll
-  for (int k2 = 0; k2 < QX; ++k2) buf[lr * F::VSX + SX::GS * k2 + p] = r[k2];
+  for (int q = 0; q < QX; ++q) mcur[q] = valid ? __ldg(mb + (long long)j0 * D + P * q) : make_float2(0.f, 0.f);
   __syncthreads();
-  for (int it = tid; it < TILE * QX; it += T) {
-    const int l2 = it / QX, k2 = it - l2 * QX;
-    float2 g[P];
-    float2* gp = buf + l2 * F::VSX + SX::GS * k2;
+  const float2* xr = xs + lr * XS + p;
+  const uint64_t keep = pol_evict_last();
+  for (int j = j0; j < j1; ++j) {
+    float2 r[QX];
 #pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-    fft_s2_fwd<P>(g);
+    for (int q = 0; q < QX; ++q) r[q] = cmul(mcur[q], xr[P * q]);
+    if (j + 1 < j1 && valid) {
 #pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
-  }
-  __syncthreads();
-  const int nrows = min(TILE, NY - rt * TILE);
-  float2* wj = a.ws + ((long long)(s % a.slots) * a.ncoils + j) * D + (long long)rt * TILE * NX;
-  for (int e = tid; e < nrows * NX; e += T) {
-    const int l3 = e / NX, pos = e - l3 * NX;
-    st_ws(wj + e, buf[l3 * F::VSX + SX::pad(pos)], pol_evict_last());
+      for (int q = 0; q < QX; ++q) mcur[q] = __ldg(mb + (long long)(j + 1) * D + P * q);
+    }
+    fft_s1_fwd<P, QX>(r, p, tx1);
+#pragma unroll
+    for (int k2 = 0; k2 < QX; ++k2) buf[lr * F::VSX + SX::GS * k2 + p] = r[k2];
+    __syncthreads();
+    for (int it = tid; it < TILE * QX; it += T) {
+      const int l2 = it / QX, k2 = it - l2 * QX;
+      float2 g[P];
+      float2* gp = buf + l2 * F::VSX + SX::GS * k2;
+      lds_group<P, SX::VEC>(g, gp);
+      fft_s2_fwd<P>(g);
+      sts_group<P, SX::VEC>(gp, g);
+    }
+    __syncthreads();
+    float2* wj = a.ws + ((long long)(s % a.slots) * a.ncoils + j) * D + (long long)rt * TILE * NX;
+    for (int e = tid; e < nvalid; e += T) {
+      const int l3 = e / NX, pos = e - l3 * NX;
+      st_ws(wj + e, buf[l3 * F::VSX + SX::pad(pos)], keep);
+    }
+    __syncthreads();
+    if (tid == 0) red_release_add(cntA + s * a.ncoils + j, 1);
   }
 }
 
@@ -170,10 +213,11 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   const float2* ty2 = sm + F::OFF_TY2;
   float2* buf = sm + F::OFF_BUF;
   float2* img = a.ws + ((long long)(s % a.slots) * a.ncoils + j) * D;
+  const uint64_t keep = pol_evict_last();
   float2 r[QY];
 #pragma unroll
   for (int q = 0; q < QY; ++q)
-    r[q] = cvalid ? ld_ws(img + (long long)(p + P * q) * NX + c0 + c, pol_evict_last()) : make_float2(0.f, 0.f);
+    r[q] = cvalid ? ld_ws(img + (long long)(p + P * q) * NX + c0 + c, keep) : make_float2(0.f, 0.f);
   fft_s1_fwd<P, QY>(r, p, ty1);
 #pragma unroll
   for (int k2 = 0; k2 < QY; ++k2) buf[c * F::VSPY + SY::GS * k2 + p] = r[k2];
@@ -194,11 +238,11 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
         const uint32_t m4 = __ldg(reinterpret_cast<const uint32_t*>(mk) + w4);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          g[4 * w4 + i] = cscale(g[4 * w4 + i], ((m4 >> (8 * i)) & 0xffu) ? a.mscale : 0.f);
+          g[4 * w4 + i] = ((m4 >> (8 * i)) & 0xffu) ? g[4 * w4 + i] : make_float2(0.f, 0.f);
       }
     } else {
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mk[k1] ? a.mscale : 0.f);
+      for (int k1 = 0; k1 < P; ++k1) g[k1] = mk[k1] ? g[k1] : make_float2(0.f, 0.f);
     }
     fft_s2_inv<P, QY>(g, k2, ty2);
 #pragma unroll
@@ -210,7 +254,7 @@ __device__ void item_colpass(const FusedArgs& a, int s, int ct, int j, float2* s
   fft_s1_inv<QY>(r);
   if (cvalid) {
 #pragma unroll
-    for (int q = 0; q < QY; ++q) st_ws(img + (long long)(p + P * q) * NX + c0 + c, r[q], pol_evict_last());
+    for (int q = 0; q < QY; ++q) st_ws(img + (long long)(p + P * q) * NX + c0 + c, r[q], keep);
   }
 }
 
@@ -221,10 +265,10 @@ __device__ __forceinline__ int atom_add_acqrel(int* p, int v) {
   return old;
 }
 
-// C(s, rt, g): coils [g*CG, g*CG + CG) of 16 rows; partial sums go to the
-// partial ring, the last group to finish a row tile sums the G partials in a
-// fixed order (deterministic) and writes the epilogue.  Returns true when this
-// item finalised the row tile.
+// C(s, rt, g): coils [g*CG, g*CG + CG) of TILE rows; workspace tiles double-buffered with
+// cp.async (L2 -> smem), maps prefetched before the FFT work; partial sums go to the
+// partial ring, the last group to finish a row tile sums the G partials in a fixed order
+// (deterministic) and writes the epilogue.  Returns true when this item finalised the tile.
 template <int P, int QY, int QX, int TILE>
 __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int CG, int* cntB,
                             int* cntT, int ncoltiles, float2* sm, int* s_flag) {
@@ -237,53 +281,70 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
   const bool valid = row < NY;
   const long long D = (long long)NX * NY;
   const float2* tx2 = sm + F::OFF_TX2;
-  float2* buf = sm + F::OFF_BUF;
+  float2* bufs = sm + F::OFF_BUF;
   const int nrows = min(TILE, NY - rt * TILE);
+  const int nvalid = nrows * NX;
   const int slot = s % a.slots;
   float2 acc[QX];
 #pragma unroll
   for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
   const int j0 = g * CG, j1 = min(a.ncoils, j0 + CG);
-  for (int j = j0; j < j1; ++j) {
-    if (tid == 0) {
-      const int* c = cntB + s * a.ncoils + j;
-      while (ld_acquire(c) < ncoltiles) __nanosleep(64);
-    }
+  auto wait_coil = [&](int j) {
+    if (tid == 0) spin_until(cntB + s * a.ncoils + j, ncoltiles, 2);
     __syncthreads();
+  };
+  auto issue_tile = [&](int j) {
     const float2* wj = a.ws + ((long long)slot * a.ncoils + j) * D + (long long)rt * TILE * NX;
-    for (int e = tid; e < nrows * NX; e += T) {
+    float2* dst = bufs + ((j - j0) & 1) * F::ROWT;
+    for (int e = 2 * tid; e < nvalid; e += 2 * T) {
       const int l3 = e / NX, pos = e - l3 * NX;
-      buf[l3 * F::VSX + SX::pad(pos)] = ld_ws(wj + e, pol_evict_first());
+      cp_async16(dst + l3 * F::VSX + SX::pad(pos), wj + e);
+    }
+    cp_async_commit();
+  };
+  wait_coil(j0);
+  issue_tile(j0);
+  for (int j = j0; j < j1; ++j) {
+    if (j + 1 < j1) {
+      wait_coil(j + 1);
+      issue_tile(j + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
+    float2* buf = bufs + ((j - j0) & 1) * F::ROWT;
+    float2 mreg[QX];
+    {
+      const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
+      const uint64_t drop = pol_evict_first();
+#pragma unroll
+      for (int q = 0; q < QX; ++q) mreg[q] = valid ? ld_ro_hint(mr + P * q, drop) : make_float2(0.f, 0.f);
+    }
     for (int it = tid; it < TILE * QX; it += T) {
       const int l2 = it / QX, k2 = it - l2 * QX;
       float2 gg[P];
       float2* gp = buf + l2 * F::VSX + SX::GS * k2;
-#pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gg[k1] = gp[k1];
+      lds_group<P, SX::VEC>(gg, gp);
       fft_s2_inv<P, QX>(gg, k2, tx2);
-#pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gp[k1] = gg[k1];
+      sts_group<P, SX::VEC>(gp, gg);
     }
     __syncthreads();
     float2 r[QX];
 #pragma unroll
     for (int k2 = 0; k2 < QX; ++k2) r[k2] = buf[lr * F::VSX + SX::GS * k2 + p];
     fft_s1_inv<QX>(r);
-    if (valid) {
-      const float2* mr = a.maps + s * a.map_bstride + (long long)j * D + (long long)row * NX + p;
 #pragma unroll
-      for (int q = 0; q < QX; ++q) cfma_conj(acc[q], ld_ro_hint(mr + P * q, pol_evict_first()), r[q]);
-    }
+    for (int q = 0; q < QX; ++q) cfma_conj(acc[q], mreg[q], r[q]);
     __syncthreads();
   }
   const long long roff = (long long)row * NX + p;
+  const uint64_t keep = pol_evict_last();
   if (G > 1) {
     float2* part = a.ws + (long long)a.slots * a.ncoils * D + ((long long)slot * G + g) * D;
     if (valid) {
 #pragma unroll
-      for (int q = 0; q < QX; ++q) st_ws(part + roff + P * q, acc[q], pol_evict_last());
+      for (int q = 0; q < QX; ++q) st_ws(part + roff + P * q, acc[q], keep);
     }
     __syncthreads();
     if (tid == 0) *s_flag = (atom_add_acqrel(cntT + s * ((NY + TILE - 1) / TILE) + rt, 1) == G - 1);
@@ -293,13 +354,16 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
 #pragma unroll
     for (int q = 0; q < QX; ++q) acc[q] = make_float2(0.f, 0.f);
     if (valid) {
+      const uint64_t drop = pol_evict_first();
       for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-        for (int q = 0; q < QX; ++q) acc[q] = cadd(acc[q], ld_ws(pb + (long long)gg * D + roff + P * q, pol_evict_first()));
+        for (int q = 0; q < QX; ++q) acc[q] = cadd(acc[q], ld_ws(pb + (long long)gg * D + roff + P * q, drop));
       }
     }
   }
   if (!valid) return true;
+#pragma unroll
+  for (int q = 0; q < QX; ++q) acc[q] = cscale(acc[q], a.oscale);
   const long long off = (long long)s * D + roff;
   if (a.coef == nullptr) {
 #pragma unroll
@@ -318,10 +382,9 @@ __device__ bool item_rowinv(const FusedArgs& a, int s, int rt, int g, int G, int
 }
 
 // ---------------------------------------------------------------- scheduler
-constexpr int COILS_PER_C = 3;  // coils per C item (partial coil sums, G = ceil(C / 3) groups)
 
 template <int P, int QY, int QX, int TILE>
-__global__ void __launch_bounds__(FusedCfg<P, QY, QX, TILE>::T, (TILE >= 16 ? 2 : 4))
+__global__ void __launch_bounds__(FusedCfg<P, QY, QX, TILE>::T, (TILE >= 16 ? 1 : 3))
 k_cart_normal_fused(FusedArgs a) {
   using F = FusedCfg<P, QY, QX, TILE>;
   constexpr int NX = F::NX, NY = F::NY, T = F::T;
@@ -331,7 +394,8 @@ k_cart_normal_fused(FusedArgs a) {
   const int S = a.batch, C = a.ncoils;
   const int nrt = (NY + TILE - 1) / TILE, nct = (NX + TILE - 1) / TILE;
   const int G = (C + COILS_PER_C - 1) / COILS_PER_C;
-  const int nA = nrt * C, nB = nct * C, nC = nrt * G;
+  const int GA = (C + COILS_PER_A - 1) / COILS_PER_A;
+  const int nA = nrt * GA, nB = nct * C, nC = nrt * G;
   const int LB = a.lagB, LC = a.lagC;
   const int R = S + LC;  // rounds
   int* rstart = reinterpret_cast<int*>(sm + F::OFF_BUF + F::BUF);  // R + 1 round offsets
@@ -367,18 +431,18 @@ k_cart_normal_fused(FusedArgs a) {
     }
     const int r = lo;
     int it = t - rstart[r];
+    const long long t_item0 = g_fused_stats ? clock64() : 0LL;
     if (r < S && it < nA) {
-      const int s = r, rt = it % nrt, j = it / nrt;
+      const int s = r, rt = it % nrt, ga = it / nrt;
       if (s >= a.slots) {  // slot reuse: every row tile of slice s - slots is final
         if (tid == 0) {
           const int* c = cntC + (s - a.slots);
-          while (ld_acquire(c) < nrt) __nanosleep(64);
+          spin_until(c, nrt, 0);
         }
         __syncthreads();
       }
-      item_rowfwd<P, QY, QX, TILE>(a, s, rt, j, sm);
-      __syncthreads();
-      if (tid == 0) red_release_add(cntA + s * C + j, 1);
+      item_rowfwd<P, QY, QX, TILE>(a, s, rt, ga * COILS_PER_A, min(C, (ga + 1) * COILS_PER_A), sm, cntA);
+      if (g_fused_stats && tid == 0) atomicAdd(g_fused_stats + 4, (unsigned long long)(clock64() - t_item0));
       continue;
     }
     if (r < S) it -= nA;
@@ -386,12 +450,13 @@ k_cart_normal_fused(FusedArgs a) {
       const int s = r - LB, ct = it % nct, j = it / nct;
       if (tid == 0) {
         const int* c = cntA + s * C + j;
-        while (ld_acquire(c) < nrt) __nanosleep(64);
+        spin_until(c, nrt, 1);
       }
       __syncthreads();
       item_colpass<P, QY, QX, TILE>(a, s, ct, j, sm);
       __syncthreads();
       if (tid == 0) red_release_add(cntB + s * C + j, 1);
+      if (g_fused_stats && tid == 0) atomicAdd(g_fused_stats + 5, (unsigned long long)(clock64() - t_item0));
       continue;
     }
     if (r >= LB && r < S + LB) it -= nB;
@@ -400,13 +465,14 @@ k_cart_normal_fused(FusedArgs a) {
       const bool fin = item_rowinv<P, QY, QX, TILE>(a, s, rt, g, G, COILS_PER_C, cntB, cntT, nct, sm, &s_flag);
       __syncthreads();
       if (fin && tid == 0) red_release_add(cntC + s, 1);
+      if (g_fused_stats && tid == 0) atomicAdd(g_fused_stats + 6, (unsigned long long)(clock64() - t_item0));
     }
     __syncthreads();
   }
 }
 
 struct FusedConfig {
-  int lagB = 1, lagC = 2, slots = 4, tile = 16;
+  int lagB = 1, lagC = 2, slots = 4, tile = 8;
 };
 FusedConfig g_cfg;
 
@@ -464,6 +530,11 @@ long long sr_fused_ws_elems(int batch, int ncoils, long long D) {
   return slots * ncoils * D + (G > 1 ? slots * G * D : 0);
 }
 
+extern "C" int sr_fused_stats(unsigned long long* dev_buf) {
+  // dev_buf: 8 device counters [spin A-slot, spin B, spin C, -, cycles A, cycles B, cycles C, -] or NULL
+  return cudaMemcpyToSymbol(g_fused_stats, &dev_buf, sizeof(dev_buf)) == cudaSuccess ? SR_OK : SR_ECUDA;
+}
+
 extern "C" int sr_fused_config(int lagB, int lagC, int slots, int tile) {
   if (lagB < 1 || lagC <= lagB || slots < lagC + 1 || slots > MAX_SLOTS || (tile != 8 && tile != 16))
     return SR_EINVAL;
@@ -478,6 +549,7 @@ int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, l
   const int slots = batch < g_cfg.slots ? batch : g_cfg.slots;
   FusedArgs a{x, anchor, maps, map_bstride, maskT, mask_bstride, out, ws, sync, batch, ncoils,
               g_cfg.lagB, g_cfg.lagC, slots < 1 ? 1 : slots, (float)(1.0 / ((double)ny * nx)), coef, u, d};
+  // defaults: tile 8 (T = 8 P threads, 3 CTAs / SM)
   if (cudaMemsetAsync(sync, 0, sizeof(int) * sr_fused_sync_ints(batch, ncoils, ny), st) != cudaSuccess)
     return SR_ECUDA;
   const int tile = fused_tile(ny, nx);

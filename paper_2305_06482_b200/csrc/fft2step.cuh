@@ -89,6 +89,47 @@ __device__ __forceinline__ void fft_s2_inv(float2* g, int k2, const float2* t2) 
 template <int Q>
 __device__ __forceinline__ void fft_s1_inv(float2* r) { RegDFT<Q, true>::run(r); }
 
+// Row-tile layout of the row passes: groups of P padded by 2 (P even) so every
+// group starts 16-byte aligned -> the step-2 group moves and the tile copies are
+// 128-bit (LDS/STS/LDG/STG.128, cp.async 16 B).  Group stride GS/2 is odd in
+// 16-byte units, so the 8-lane phases of the 128-bit step-2 accesses are
+// conflict-free; VS = P (mod 16) keeps the 64-bit step-1 stores conflict-free.
+template <int P_, int Q_>
+struct RowShape {
+  static constexpr int P = P_, Q = Q_, N = P_ * Q_;
+  static constexpr bool VEC = (P_ % 2 == 0) && (P_ > 1);
+  static constexpr int GS = VEC ? P_ + 2 : (P_ == 1 ? 1 : P_ + 1);
+  static constexpr int VS0 = Q_ * GS;
+  static constexpr int VS = VS0 + ((((P_ % 16) - (VS0 % 16)) % 16 + 16) % 16);
+  __device__ __forceinline__ static int pad(int pos) { return (P_ == 1) ? pos : pos + (GS - P_) * (pos / P_); }
+};
+
+template <int P, bool VEC>
+__device__ __forceinline__ void lds_group(float2* g, const float2* gp) {
+  if constexpr (VEC) {
+#pragma unroll
+    for (int i = 0; i < P / 2; ++i) {
+      const float4 v = reinterpret_cast<const float4*>(gp)[i];
+      g[2 * i] = make_float2(v.x, v.y);
+      g[2 * i + 1] = make_float2(v.z, v.w);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) g[i] = gp[i];
+  }
+}
+template <int P, bool VEC>
+__device__ __forceinline__ void sts_group(float2* gp, const float2* g) {
+  if constexpr (VEC) {
+#pragma unroll
+    for (int i = 0; i < P / 2; ++i)
+      reinterpret_cast<float4*>(gp)[i] = make_float4(g[2 * i].x, g[2 * i].y, g[2 * i + 1].x, g[2 * i + 1].y);
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) gp[i] = g[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Supported lengths and their (P, Q) split.  X(N, P, Q)
 #define SR_FFT_SIZES(X)                                                          \

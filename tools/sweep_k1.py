@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--chunks", default="0,32,16")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--fused", default="", help="semicolon list of lagB,lagC,slots,tile configs of the persistent launch")
+    ap.add_argument("--stats", action="store_true", help="collect fused-kernel wait/item statistics")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     w = bench.build_workload(0, dev)
@@ -35,8 +36,15 @@ def main():
         kern._ws = None
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=-1), args.steps, 3, torch.cuda.synchronize)
         ms = t / args.steps * 1e3
-        print(json.dumps({"fused": cfg, "ms_per_apply": ms,
-                          "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}), flush=True)
+        rec = {"fused": cfg, "ms_per_apply": ms, "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}
+        if args.stats:
+            st = torch.zeros(8, dtype=torch.int64, device=dev)
+            _lib.call("sr_fused_stats", st.data_ptr())
+            kern.normal(smaps, x, out, chunk=-1)
+            torch.cuda.synchronize()
+            _lib.call("sr_fused_stats", None)
+            rec["stats"] = st.cpu().tolist()
+        print(json.dumps(rec), flush=True)
     for ch in [int(c) for c in args.chunks.split(",") if c]:
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=ch), args.steps, 3, torch.cuda.synchronize)
         ms = t / args.steps * 1e3
