@@ -162,22 +162,27 @@ int sr_scalar_op(int op, const double* in0, const double* in1, double* state, fl
  *   base (3, N) int32 = ceil(u - w/2) per axis (fp64 on the host), frac (3, N) fp32 = u - base;
  *   wgt: w (normal) or sqrt(w) (forward / adjoint) per sample, NULL = 1; orig: original
  *   index of each (locality-sorted) sample or NULL; grids: ncoils*G (fwd/adj) or
- *   2*ncoils*G (normal) complex64 workspace.  Epilogue coef/u/d as sr_cart_normal. */
+ *   2*ncoils*G (normal) complex64 workspace.  Epilogue coef/u/d as sr_cart_normal.
+ *   chunks (nchunks x 5 int32: bin origin (3 grid indices), first sorted sample, count <= 256)
+ *   selects the binned shared-memory gridding with bins of binsize^d cells; chunks = NULL
+ *   uses one thread per sample with global float2 atomics.  With chunks, partial has
+ *   nchunks entries (forward with ymeas), else sr_nufft_partial_blocks(N). */
 int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
                     const int* dims, const int* gdims, const float* betas, int width,
                     const float* ia0, const float* ia1, const float* ia2, const int* base,
                     const float* frac, const float* wgt, long long nsamples, sr_c64* out,
-                    sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+                    sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, const int* chunks,
+                    int nchunks, int binsize, void* stream);
 int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int* dims, const int* gdims,
                      const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
                      const int* base, const float* frac, const float* sqrtw, const int* orig,
                      long long nsamples, sr_c64* y, const sr_c64* ymeas, double* partial, sr_c64* grids,
-                     void* stream);
+                     const int* chunks, int nchunks, int binsize, void* stream);
 int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int* dims, const int* gdims,
                      const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
                      const int* base, const float* frac, const float* sqrtw, const int* orig,
                      long long nsamples, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
-                     const sr_c64* d, void* stream);
+                     const sr_c64* d, const int* chunks, int nchunks, int binsize, void* stream);
 int sr_nufft_partial_blocks(long long nsamples);
 /* Batched unnormalised FFT along the middle axis of an [outer][n][inner] array, in
  * place: inv = 0 natural -> perm order, inv = 1 perm -> natural. */

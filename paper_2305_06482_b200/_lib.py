@@ -42,11 +42,11 @@ SIGNATURES = {
     "sr_fused_config": [_i, _i, _i, _i],
     "sr_fused_stats": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
-                        _vp, _vp, _vp, _vp],
+                        _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_forward": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
-                         _vp, _vp, _vp],
+                         _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_adjoint": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
-                         _vp, _vp, _vp, _vp],
+                         _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_partial_blocks": [_ll],
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
     "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],

@@ -455,6 +455,176 @@ k_nufft_samples(int mode, const float2* __restrict__ src, float2* __restrict__ d
   }
 }
 
+// ----------------------------------------------------------------- binned gridding
+// Samples sorted by the tile (bin) of their first tap; one CTA per chunk of <= BIN_CHUNK
+// samples of one bin.  The CTA stages the bin's (B + w - 1)^d spectrum tile in shared
+// memory (interp reads), accumulates the spread into a shared tile (shared atomics) and
+// flushes it with one global float2 atomic per cell: ~ (1 + (w-1)/B)^d global accesses
+// per grid cell instead of w^d per sample.  KB weights are computed once per sample into
+// shared memory and reused for every coil.
+constexpr int BIN_CHUNK = 256;
+constexpr int BIN_THREADS = 256;
+
+template <int MODE>  // 0 normal (interp, *w, spread), 1 forward (interp -> y), 2 adjoint (spread y)
+__global__ void __launch_bounds__(BIN_THREADS)
+k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int* __restrict__ base,
+             const float* __restrict__ frac, const float* __restrict__ wgt, const int* __restrict__ orig,
+             long long N, const int* __restrict__ chunks, NufftGeom g, int B, int ncoils, float scale,
+             float2* __restrict__ y, const float2* __restrict__ ymeas, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int w = g.width;
+  int tb[3], act[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    act[a] = g.n[a] > 1;
+    tb[a] = act[a] ? B + w - 1 : 1;
+  }
+  const int cells = tb[0] * tb[1] * tb[2];
+  float2* tile = reinterpret_cast<float2*>(smraw);                  // spectrum tile (modes 0, 1)
+  float2* acc = tile + ((MODE == 2) ? 0 : cells);                    // spread accumulator (modes 0, 2)
+  float* wts = reinterpret_cast<float*>(acc + ((MODE == 1) ? 0 : cells));  // [3][w][BIN_CHUNK]
+  short* loc = reinterpret_cast<short*>(wts + 3 * MAXW * BIN_CHUNK);       // [3][BIN_CHUNK]
+  const int* ch = chunks + 5 * blockIdx.x;
+  const int org[3] = {ch[0], ch[1], ch[2]};
+  const int s0 = ch[3], ns = ch[4];
+  const int tid = threadIdx.x;
+  // per-sample weights and local tap origins
+  for (int i = tid; i < ns; i += BIN_THREADS) {
+    const long long sidx = s0 + i;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (!act[a]) {
+        loc[a * BIN_CHUNK + i] = 0;
+        for (int k = 0; k < MAXW; ++k) wts[(a * MAXW + k) * BIN_CHUNK + i] = (k == 0) ? 1.f : 0.f;
+        continue;
+      }
+      int b = base[a * N + sidx] % g.g[a];
+      if (b < 0) b += g.g[a];
+      int l = b - org[a];
+      if (l < 0) l += g.g[a];
+      loc[a * BIN_CHUNK + i] = (short)l;
+      const float t = frac[a * N + sidx];
+      for (int k = 0; k < MAXW; ++k)
+        wts[(a * MAXW + k) * BIN_CHUNK + i] = (k < w) ? kb_weight(t - (float)k, g.beta[a], (float)w) : 0.f;
+    }
+  }
+  const int w0 = act[0] ? w : 1, w1 = act[1] ? w : 1, w2 = act[2] ? w : 1;
+  double acc2 = 0.0;
+  for (int j = 0; j < ncoils; ++j) {
+    const long long go = (long long)j * g.G;
+    __syncthreads();
+    for (int e = tid; e < cells; e += BIN_THREADS) {
+      const int c2 = e % tb[2];
+      const int c1 = (e / tb[2]) % tb[1];
+      const int c0 = e / (tb[2] * tb[1]);
+      if (MODE != 2) {
+        const int k0 = (org[0] + c0) % g.g[0], k1 = (org[1] + c1) % g.g[1], k2 = (org[2] + c2) % g.g[2];
+        const long long off = (long long)perm_of(k0, g.P[0], g.Q[0]) * g.g[1] * g.g[2] +
+                              (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] + perm_of(k2, g.P[2], g.Q[2]);
+        tile[e] = src[go + off];
+      }
+      if (MODE != 1) acc[e] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int i = tid; i < ns; i += BIN_THREADS) {
+      const int l0 = loc[i], l1 = loc[BIN_CHUNK + i], l2 = loc[2 * BIN_CHUNK + i];
+      float2 v = make_float2(0.f, 0.f);
+      const long long sidx = s0 + i;
+      const long long oi = orig ? orig[sidx] : sidx;
+      if (MODE != 2) {
+        for (int a0 = 0; a0 < w0; ++a0) {
+          const float wa = wts[a0 * BIN_CHUNK + i];
+          for (int a1 = 0; a1 < w1; ++a1) {
+            const float wb = wa * wts[(MAXW + a1) * BIN_CHUNK + i];
+            const float2* row = tile + ((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2;
+            for (int a2 = 0; a2 < w2; ++a2) {
+              const float wt = wb * wts[(2 * MAXW + a2) * BIN_CHUNK + i];
+              const float2 sv = row[a2];
+              v.x = fmaf(wt, sv.x, v.x);
+              v.y = fmaf(wt, sv.y, v.y);
+            }
+          }
+        }
+      }
+      const float wi = wgt ? wgt[sidx] : 1.f;
+      if (MODE == 1) {
+        float2 yv = cscale(v, wi * scale);
+        if (ymeas) {
+          yv = csub(yv, ymeas[(long long)j * N + oi]);
+          acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
+        }
+        y[(long long)j * N + oi] = yv;
+        continue;
+      }
+      if (MODE == 0) v = cscale(v, wi * scale);
+      else v = cscale(y[(long long)j * N + oi], wi * scale);
+      for (int a0 = 0; a0 < w0; ++a0) {
+        const float wa = wts[a0 * BIN_CHUNK + i];
+        for (int a1 = 0; a1 < w1; ++a1) {
+          const float wb = wa * wts[(MAXW + a1) * BIN_CHUNK + i];
+          float2* row = acc + ((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2;
+          for (int a2 = 0; a2 < w2; ++a2) {
+            const float wt = wb * wts[(2 * MAXW + a2) * BIN_CHUNK + i];
+            atomicAdd(&row[a2].x, v.x * wt);
+            atomicAdd(&row[a2].y, v.y * wt);
+          }
+        }
+      }
+    }
+    if (MODE != 1) {
+      __syncthreads();
+      for (int e = tid; e < cells; e += BIN_THREADS) {
+        const float2 av = acc[e];
+        if (av.x == 0.f && av.y == 0.f) continue;
+        const int c2 = e % tb[2];
+        const int c1 = (e / tb[2]) % tb[1];
+        const int c0 = e / (tb[2] * tb[1]);
+        const int k0 = (org[0] + c0) % g.g[0], k1 = (org[1] + c1) % g.g[1], k2 = (org[2] + c2) % g.g[2];
+        const long long off = (long long)perm_of(k0, g.P[0], g.Q[0]) * g.g[1] * g.g[2] +
+                              (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] + perm_of(k2, g.P[2], g.Q[2]);
+        red_add_f2(dst + go + off, av);
+      }
+    }
+  }
+  if (MODE == 1 && partial) {
+    __shared__ double red[BIN_THREADS];
+    red[tid] = acc2;
+    __syncthreads();
+    for (int st = BIN_THREADS / 2; st > 0; st >>= 1) {
+      if (tid < st) red[tid] += red[tid + st];
+      __syncthreads();
+    }
+    if (tid == 0) partial[blockIdx.x] = red[0];
+  }
+}
+
+size_t bin_smem(const NufftGeom& g, int B, int mode) {
+  long long cells = 1;
+  for (int a = 0; a < 3; ++a) cells *= (g.n[a] > 1) ? (B + g.width - 1) : 1;
+  const long long tiles = (mode == 0) ? 2 : 1;
+  return (size_t)(sizeof(float2) * cells * tiles + sizeof(float) * 3 * MAXW * BIN_CHUNK +
+                  sizeof(short) * 3 * BIN_CHUNK + 16);
+}
+
+template <int MODE>
+int launch_bins(const float2* src, float2* dst, const int* base, const float* frac, const float* wgt,
+                const int* orig, long long N, const int* chunks, int nchunks, const NufftGeom& g, int B,
+                int ncoils, float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
+  const size_t smem = bin_smem(g, B, MODE);
+  static size_t configured = 0;
+  if (smem > configured) {
+    if (cudaFuncSetAttribute(k_nufft_bins<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return SR_ECUDA;
+    configured = smem;
+  }
+  if (nchunks < 1) return SR_OK;
+  k_nufft_bins<MODE><<<nchunks, BIN_THREADS, smem, st>>>(src, dst, base, frac, wgt, orig, N, chunks, g, B, ncoils,
+                                                         scale, y, ymeas, partial);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
 int grid_fft(float2* grid, const NufftGeom& g, int ncoils, int inv, cudaStream_t st) {
   // axis 2 (contiguous), axis 1 ([C*g0][g1][g2]), axis 0 ([C][g0][g1*g2])
   int rc = fft_axis(grid, (long long)ncoils * g.g[0] * g.g[1], g.g[2], 1, inv, st);
@@ -507,7 +677,8 @@ int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, i
                     const int* dims, const int* gdims, const float* betas, int width,
                     const float* ia0, const float* ia1, const float* ia2, const int* base,
                     const float* frac, const float* wgt, long long nsamples, sr_c64* out,
-                    sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, void* stream) {
+                    sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, const int* chunks,
+                    int nchunks, int binsize, void* stream) {
   NufftGeom g;
   if (!make_geom(dims, gdims, betas, width, g) || ncoils < 1) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -519,10 +690,16 @@ int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, i
   int rc = grid_fft(src, g, ncoils, 0, st);
   if (rc) return rc;
   if (cudaMemsetAsync(dst, 0, sizeof(float2) * ncoils * g.G, st) != cudaSuccess) return SR_ECUDA;
-  k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(0, src, dst, base, frac, wgt, nullptr, nsamples,
-                                                           g, ncoils, (float)(1.0 / (double)g.D), nullptr,
-                                                           nullptr, nullptr);
-  SR_CHECK_LAUNCH();
+  if (chunks) {
+    rc = launch_bins<0>(src, dst, base, frac, wgt, nullptr, nsamples, chunks, nchunks, g, binsize, ncoils,
+                        (float)(1.0 / (double)g.D), nullptr, nullptr, nullptr, st);
+    if (rc) return rc;
+  } else {
+    k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(0, src, dst, base, frac, wgt, nullptr, nsamples,
+                                                             g, ncoils, (float)(1.0 / (double)g.D), nullptr,
+                                                             nullptr, nullptr);
+    SR_CHECK_LAUNCH();
+  }
   rc = grid_fft(dst, g, ncoils, 1, st);
   if (rc) return rc;
   k_nufft_crop<<<148 * 8, 256, 0, st>>>(dst, (const float2*)maps, ia0, ia1, ia2, (float2*)out, g, ncoils, 1.f,
@@ -538,7 +715,7 @@ int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int*
                      const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
                      const int* base, const float* frac, const float* sqrtw, const int* orig,
                      long long nsamples, sr_c64* y, const sr_c64* ymeas, double* partial, sr_c64* grids,
-                     void* stream) {
+                     const int* chunks, int nchunks, int binsize, void* stream) {
   NufftGeom g;
   if (!make_geom(dims, gdims, betas, width, g) || ncoils < 1) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -548,6 +725,9 @@ int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int*
   SR_CHECK_LAUNCH();
   int rc = grid_fft(src, g, ncoils, 0, st);
   if (rc) return rc;
+  if (chunks)
+    return launch_bins<1>(src, nullptr, base, frac, sqrtw, orig, nsamples, chunks, nchunks, g, binsize, ncoils,
+                          (float)(1.0 / sqrt((double)g.D)), (float2*)y, (const float2*)ymeas, partial, st);
   k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(1, src, nullptr, base, frac, sqrtw, orig, nsamples,
                                                            g, ncoils, (float)(1.0 / sqrt((double)g.D)),
                                                            (float2*)y, (const float2*)ymeas, partial);
@@ -560,16 +740,22 @@ int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int*
                      const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
                      const int* base, const float* frac, const float* sqrtw, const int* orig,
                      long long nsamples, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
-                     const sr_c64* d, void* stream) {
+                     const sr_c64* d, const int* chunks, int nchunks, int binsize, void* stream) {
   NufftGeom g;
   if (!make_geom(dims, gdims, betas, width, g) || ncoils < 1) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   float2* dst = (float2*)grids;
   if (cudaMemsetAsync(dst, 0, sizeof(float2) * ncoils * g.G, st) != cudaSuccess) return SR_ECUDA;
-  k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(2, nullptr, dst, base, frac, sqrtw, orig, nsamples,
-                                                           g, ncoils, (float)(1.0 / sqrt((double)g.D)),
-                                                           (float2*)y, nullptr, nullptr);
-  SR_CHECK_LAUNCH();
+  if (chunks) {
+    int rc0 = launch_bins<2>(nullptr, dst, base, frac, sqrtw, orig, nsamples, chunks, nchunks, g, binsize, ncoils,
+                             (float)(1.0 / sqrt((double)g.D)), (float2*)y, nullptr, nullptr, st);
+    if (rc0) return rc0;
+  } else {
+    k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(2, nullptr, dst, base, frac, sqrtw, orig, nsamples,
+                                                             g, ncoils, (float)(1.0 / sqrt((double)g.D)),
+                                                             (float2*)y, nullptr, nullptr);
+    SR_CHECK_LAUNCH();
+  }
   int rc = grid_fft(dst, g, ncoils, 1, st);
   if (rc) return rc;
   // the 1/sqrt(D) scale was applied with the spread

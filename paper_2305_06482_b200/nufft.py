@@ -44,7 +44,10 @@ def kb_apodization(r_over_g: np.ndarray, width: int, beta: float) -> np.ndarray:
 class GriddedKernel:
     """Device NUFFT plan for one image grid (2-D or 3-D)."""
 
-    def __init__(self, dims, points, oversamp: float = 1.25, width: int = 6):
+    BIN_CHUNK = 256  # samples per CTA of the binned gridding kernels (nufft.cu)
+
+    def __init__(self, dims, points, oversamp: float = 1.25, width: int = 6, binned: bool = True,
+                 binsize: int | None = None):
         self.dims = tuple(int(n) for n in dims)
         nd = len(self.dims)
         if nd not in (2, 3):
@@ -73,10 +76,32 @@ class GriddedKernel:
             b = np.ceil(u - w / 2.0)
             bases.append(b.astype(np.int64))
             fracs.append(u - b)
-        # locality order: coarse 8-bin tiles, row-major
-        keys = [bases[a] // 8 for a in range(nd)][::-1]
-        order = np.lexsort(keys)
+        # bins: tile of binsize^d grid cells holding each sample's first tap; samples sorted by bin
+        self.binsize = int(binsize or (8 if nd == 3 else 16))
+        B = self.binsize
+        bpos = [np.mod(bases[a], g) for a, g in enumerate(self.gdims)]
+        nbins = [-(-g // B) for g in self.gdims]
+        binid = np.zeros(self.n_points, dtype=np.int64)
+        for a in range(nd):
+            binid = binid * nbins[a] + bpos[a] // B
+        order = np.argsort(binid, kind="stable")
         self.order = order
+        chunks = []
+        if self.n_points:
+            sb = binid[order]
+            starts = np.flatnonzero(np.r_[True, sb[1:] != sb[:-1]])
+            ends = np.r_[starts[1:], self.n_points]
+            for st, en in zip(starts, ends):
+                bid = int(sb[st])
+                coords = []
+                for a in range(nd - 1, -1, -1):
+                    coords.append((bid % nbins[a]) * B)
+                    bid //= nbins[a]
+                coords = [0] * (3 - nd) + coords[::-1]
+                for c0 in range(st, en, self.BIN_CHUNK):
+                    chunks.append(coords + [c0, min(self.BIN_CHUNK, en - c0)])
+        self.binned = bool(binned)
+        self.nchunks = len(chunks)
         pad = 3 - nd
         base3 = np.zeros((3, self.n_points), dtype=np.int32)
         frac3 = np.zeros((3, self.n_points), dtype=np.float32)
@@ -99,9 +124,10 @@ class GriddedKernel:
             r = np.arange(n, dtype=np.float64) - n // 2
             ia.append(1.0 / kb_apodization(r / g, self.width, beta))
         self.ia = [dv.host_to_dev(v.astype(np.float32), torch.float32, dev) for v in ia]
+        self.chunks = dv.host_to_dev(np.asarray(chunks, dtype=np.int32).reshape(-1, 5), torch.int32, dev)
         self._grids = None
         self._wcache: dict = {}
-        self.nparts = _lib.lib().sr_nufft_partial_blocks(self.n_points)
+        self.nparts = max(_lib.lib().sr_nufft_partial_blocks(self.n_points), self.nchunks)
 
     # ------------------------------------------------------------ helpers
     def workspace(self, ncoils: int, batch: int | None = None, chunk: int = 0, normal: bool = True):
@@ -137,13 +163,19 @@ class GriddedKernel:
     def partial_shape(self, ncoils: int) -> tuple:
         return (1, self.nparts)
 
+    def _bins(self):
+        if self.binned:
+            return dv.ptr(self.chunks), self.nchunks, self.binsize
+        return None, 0, 0
+
     # ------------------------------------------------------------ device API
     def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None, chunk=None):
         C = self._maps(maps)
         grids = self.workspace(C, normal=True)
         _lib.call("sr_nufft_normal", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), C, *self._geom()[:4],
                   *self._geom()[4:], dv.ptr(self.base), dv.ptr(self.frac), dv.ptr(self._weights(w, True)),
-                  self.n_points, dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), dv.stream())
+                  self.n_points, dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), *self._bins(),
+                  dv.stream())
         return out
 
     def forward(self, maps, x, y=None, *, ymeas=None, partial=None, partial_blocks=None, w=None):
@@ -155,7 +187,7 @@ class GriddedKernel:
         grids = self.workspace(C, normal=False)
         _lib.call("sr_nufft_forward", dv.ptr(x), dv.ptr(maps), C, *self._geom(), dv.ptr(self.base),
                   dv.ptr(self.frac), dv.ptr(self._weights(w, False)), dv.ptr(self.orig), self.n_points,
-                  dv.ptr(y), dv.ptr(ymeas), dv.ptr(partial), dv.ptr(grids), dv.stream())
+                  dv.ptr(y), dv.ptr(ymeas), dv.ptr(partial), dv.ptr(grids), *self._bins(), dv.stream())
         return y
 
     def adjoint(self, maps, y, out, *, coef=None, u=None, d=None, w=None):
@@ -163,7 +195,7 @@ class GriddedKernel:
         grids = self.workspace(C, normal=False)
         _lib.call("sr_nufft_adjoint", dv.ptr(y), dv.ptr(maps), C, *self._geom(), dv.ptr(self.base),
                   dv.ptr(self.frac), dv.ptr(self._weights(w, False)), dv.ptr(self.orig), self.n_points,
-                  dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), dv.stream())
+                  dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), *self._bins(), dv.stream())
         return out
 
     # ------------------------------------------------- reference plugin protocol
