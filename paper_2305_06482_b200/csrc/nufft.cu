@@ -302,6 +302,19 @@ __device__ __forceinline__ void sample_taps(const NufftGeom& g, const int* __res
   }
 }
 
+// shared-memory float2 accumulate: one 64-bit CAS per update (no native shared FADD)
+__device__ __forceinline__ void smem_add_f2(float2* p, float2 v) {
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+  unsigned long long old = *q, assumed;
+  do {
+    assumed = old;
+    float2 cur = *reinterpret_cast<float2*>(&assumed);
+    cur.x += v.x;
+    cur.y += v.y;
+    old = atomicCAS(q, assumed, *reinterpret_cast<unsigned long long*>(&cur));
+  } while (old != assumed);
+}
+
 __device__ __forceinline__ void red_add_f2(float2* p, float2 v) {
   atomicAdd(p, v);  // sm_90+: vector float2 atomic add
 }
@@ -509,6 +522,9 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
     }
   }
   const int w0 = act[0] ? w : 1, w1 = act[1] ? w : 1, w2 = act[2] ? w : 1;
+  const int ntaps = w0 * w1 * w2;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = BIN_THREADS / 32;
   double acc2 = 0.0;
   for (int j = 0; j < ncoils; ++j) {
     const long long go = (long long)j * g.G;
@@ -526,49 +542,47 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
       if (MODE != 1) acc[e] = make_float2(0.f, 0.f);
     }
     __syncthreads();
-    for (int i = tid; i < ns; i += BIN_THREADS) {
+    // one warp per sample, lanes over the w^d taps: no two lanes of a warp touch the same
+    // cell, so the shared accumulator only sees (rare) contention between the 8 warps
+    for (int i = warp; i < ns; i += NWARPS) {
       const int l0 = loc[i], l1 = loc[BIN_CHUNK + i], l2 = loc[2 * BIN_CHUNK + i];
-      float2 v = make_float2(0.f, 0.f);
       const long long sidx = s0 + i;
       const long long oi = orig ? orig[sidx] : sidx;
+      float2 v = make_float2(0.f, 0.f);
       if (MODE != 2) {
-        for (int a0 = 0; a0 < w0; ++a0) {
-          const float wa = wts[a0 * BIN_CHUNK + i];
-          for (int a1 = 0; a1 < w1; ++a1) {
-            const float wb = wa * wts[(MAXW + a1) * BIN_CHUNK + i];
-            const float2* row = tile + ((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2;
-            for (int a2 = 0; a2 < w2; ++a2) {
-              const float wt = wb * wts[(2 * MAXW + a2) * BIN_CHUNK + i];
-              const float2 sv = row[a2];
-              v.x = fmaf(wt, sv.x, v.x);
-              v.y = fmaf(wt, sv.y, v.y);
-            }
-          }
+        for (int t = lane; t < ntaps; t += 32) {
+          const int a2 = t % w2, a1 = (t / w2) % w1, a0 = t / (w2 * w1);
+          const float wt = wts[a0 * BIN_CHUNK + i] * wts[(MAXW + a1) * BIN_CHUNK + i] *
+                           wts[(2 * MAXW + a2) * BIN_CHUNK + i];
+          const float2 sv = tile[((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2 + a2];
+          v.x = fmaf(wt, sv.x, v.x);
+          v.y = fmaf(wt, sv.y, v.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+          v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
         }
       }
       const float wi = wgt ? wgt[sidx] : 1.f;
       if (MODE == 1) {
-        float2 yv = cscale(v, wi * scale);
-        if (ymeas) {
-          yv = csub(yv, ymeas[(long long)j * N + oi]);
-          acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
+        if (lane == 0) {
+          float2 yv = cscale(v, wi * scale);
+          if (ymeas) {
+            yv = csub(yv, ymeas[(long long)j * N + oi]);
+            acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
+          }
+          y[(long long)j * N + oi] = yv;
         }
-        y[(long long)j * N + oi] = yv;
         continue;
       }
       if (MODE == 0) v = cscale(v, wi * scale);
       else v = cscale(y[(long long)j * N + oi], wi * scale);
-      for (int a0 = 0; a0 < w0; ++a0) {
-        const float wa = wts[a0 * BIN_CHUNK + i];
-        for (int a1 = 0; a1 < w1; ++a1) {
-          const float wb = wa * wts[(MAXW + a1) * BIN_CHUNK + i];
-          float2* row = acc + ((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2;
-          for (int a2 = 0; a2 < w2; ++a2) {
-            const float wt = wb * wts[(2 * MAXW + a2) * BIN_CHUNK + i];
-            atomicAdd(&row[a2].x, v.x * wt);
-            atomicAdd(&row[a2].y, v.y * wt);
-          }
-        }
+      for (int t = lane; t < ntaps; t += 32) {
+        const int a2 = t % w2, a1 = (t / w2) % w1, a0 = t / (w2 * w1);
+        const float wt = wts[a0 * BIN_CHUNK + i] * wts[(MAXW + a1) * BIN_CHUNK + i] *
+                         wts[(2 * MAXW + a2) * BIN_CHUNK + i];
+        smem_add_f2(&acc[((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2 + a2], cscale(v, wt));
       }
     }
     if (MODE != 1) {
