@@ -478,85 +478,97 @@ k_nufft_samples(int mode, const float2* __restrict__ src, float2* __restrict__ d
 constexpr int BIN_CHUNK = 256;
 constexpr int BIN_THREADS = 256;
 
-template <int MODE>  // 0 normal (interp, *w, spread), 1 forward (interp -> y), 2 adjoint (spread y)
+template <int ND, int W, int B>
+struct BinCfg {
+  static constexpr int TB = B + W - 1;                       // tile extent per active axis
+  static constexpr int T0 = (ND == 3) ? TB : 1, T1 = TB, T2 = TB;
+  static constexpr int CELLS = T0 * T1 * T2;
+  static constexpr int NTAPS = (ND == 3 ? W : 1) * W * W;
+};
+
+// 0 normal (interp, *w, spread), 1 forward (interp -> y), 2 adjoint (spread y).
+// One warp per sample, lanes over the W^ND taps: no two lanes of a warp touch the
+// same cell, so the shared accumulator only sees contention between the 8 warps.
+template <int MODE, int ND, int W, int B>
 __global__ void __launch_bounds__(BIN_THREADS)
 k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int* __restrict__ base,
              const float* __restrict__ frac, const float* __restrict__ wgt, const int* __restrict__ orig,
-             long long N, const int* __restrict__ chunks, NufftGeom g, int B, int ncoils, float scale,
+             long long N, const int* __restrict__ chunks, NufftGeom g, int ncoils, float scale,
              float2* __restrict__ y, const float2* __restrict__ ymeas, double* __restrict__ partial) {
+  using C = BinCfg<ND, W, B>;
+  constexpr int CELLS = C::CELLS, T1 = C::T1, T2 = C::T2, NTAPS = C::NTAPS;
+  constexpr int A0 = 3 - ND;  // first active axis
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int w = g.width;
-  int tb[3], act[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    act[a] = g.n[a] > 1;
-    tb[a] = act[a] ? B + w - 1 : 1;
-  }
-  const int cells = tb[0] * tb[1] * tb[2];
-  float2* tile = reinterpret_cast<float2*>(smraw);                  // spectrum tile (modes 0, 1)
-  float2* acc = tile + ((MODE == 2) ? 0 : cells);                    // spread accumulator (modes 0, 2)
-  float* wts = reinterpret_cast<float*>(acc + ((MODE == 1) ? 0 : cells));  // [3][w][BIN_CHUNK]
-  short* loc = reinterpret_cast<short*>(wts + 3 * MAXW * BIN_CHUNK);       // [3][BIN_CHUNK]
+  float2* tile = reinterpret_cast<float2*>(smraw);                       // spectrum tile (modes 0, 1)
+  float2* acc = tile + ((MODE == 2) ? 0 : CELLS);                         // spread accumulator (0, 2)
+  float* wts = reinterpret_cast<float*>(acc + ((MODE == 1) ? 0 : CELLS));  // [3][W][BIN_CHUNK]
+  short* loc = reinterpret_cast<short*>(wts + 3 * W * BIN_CHUNK);          // [3][BIN_CHUNK]
   const int* ch = chunks + 5 * blockIdx.x;
-  const int org[3] = {ch[0], ch[1], ch[2]};
+  const int org0 = ch[0], org1 = ch[1], org2 = ch[2];
   const int s0 = ch[3], ns = ch[4];
   const int tid = threadIdx.x;
-  // per-sample weights and local tap origins
+  const long long sg12 = (long long)g.g[1] * g.g[2];
+  // per-sample KB weights and local tap origins (once, reused by every coil)
   for (int i = tid; i < ns; i += BIN_THREADS) {
     const long long sidx = s0 + i;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      if (!act[a]) {
+      if (a < A0) {
         loc[a * BIN_CHUNK + i] = 0;
-        for (int k = 0; k < MAXW; ++k) wts[(a * MAXW + k) * BIN_CHUNK + i] = (k == 0) ? 1.f : 0.f;
+#pragma unroll
+        for (int k = 0; k < W; ++k) wts[(a * W + k) * BIN_CHUNK + i] = (k == 0) ? 1.f : 0.f;
         continue;
       }
-      int b = base[a * N + sidx] % g.g[a];
-      if (b < 0) b += g.g[a];
-      int l = b - org[a];
+      int bb = base[a * N + sidx] % g.g[a];
+      if (bb < 0) bb += g.g[a];
+      int l = bb - (a == 0 ? org0 : (a == 1 ? org1 : org2));
       if (l < 0) l += g.g[a];
       loc[a * BIN_CHUNK + i] = (short)l;
       const float t = frac[a * N + sidx];
-      for (int k = 0; k < MAXW; ++k)
-        wts[(a * MAXW + k) * BIN_CHUNK + i] = (k < w) ? kb_weight(t - (float)k, g.beta[a], (float)w) : 0.f;
+#pragma unroll
+      for (int k = 0; k < W; ++k) wts[(a * W + k) * BIN_CHUNK + i] = kb_weight(t - (float)k, g.beta[a], (float)W);
     }
   }
-  const int w0 = act[0] ? w : 1, w1 = act[1] ? w : 1, w2 = act[2] ? w : 1;
-  const int ntaps = w0 * w1 * w2;
+  auto cell_off = [&](int e) -> long long {
+    const int c2 = e % T2, c1 = (e / T2) % T1, c0 = e / (T2 * T1);
+    int k0 = org0 + c0, k1 = org1 + c1, k2 = org2 + c2;
+    k0 -= (k0 >= g.g[0]) ? g.g[0] : 0;
+    k1 -= (k1 >= g.g[1]) ? g.g[1] : 0;
+    k2 -= (k2 >= g.g[2]) ? g.g[2] : 0;
+    if (k0 >= g.g[0]) k0 %= g.g[0];  // tiles wider than the grid (tiny grids)
+    if (k1 >= g.g[1]) k1 %= g.g[1];
+    if (k2 >= g.g[2]) k2 %= g.g[2];
+    return (long long)perm_of(k0, g.P[0], g.Q[0]) * sg12 + (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] +
+           perm_of(k2, g.P[2], g.Q[2]);
+  };
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = BIN_THREADS / 32;
   double acc2 = 0.0;
   for (int j = 0; j < ncoils; ++j) {
     const long long go = (long long)j * g.G;
     __syncthreads();
-    for (int e = tid; e < cells; e += BIN_THREADS) {
-      const int c2 = e % tb[2];
-      const int c1 = (e / tb[2]) % tb[1];
-      const int c0 = e / (tb[2] * tb[1]);
-      if (MODE != 2) {
-        const int k0 = (org[0] + c0) % g.g[0], k1 = (org[1] + c1) % g.g[1], k2 = (org[2] + c2) % g.g[2];
-        const long long off = (long long)perm_of(k0, g.P[0], g.Q[0]) * g.g[1] * g.g[2] +
-                              (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] + perm_of(k2, g.P[2], g.Q[2]);
-        tile[e] = src[go + off];
-      }
+    for (int e = tid; e < CELLS; e += BIN_THREADS) {
+      if (MODE != 2) tile[e] = src[go + cell_off(e)];
       if (MODE != 1) acc[e] = make_float2(0.f, 0.f);
     }
     __syncthreads();
-    // one warp per sample, lanes over the w^d taps: no two lanes of a warp touch the same
-    // cell, so the shared accumulator only sees (rare) contention between the 8 warps
     for (int i = warp; i < ns; i += NWARPS) {
       const int l0 = loc[i], l1 = loc[BIN_CHUNK + i], l2 = loc[2 * BIN_CHUNK + i];
+      const int cbase = (l0 * T1 + l1) * T2 + l2;
       const long long sidx = s0 + i;
-      const long long oi = orig ? orig[sidx] : sidx;
       float2 v = make_float2(0.f, 0.f);
       if (MODE != 2) {
-        for (int t = lane; t < ntaps; t += 32) {
-          const int a2 = t % w2, a1 = (t / w2) % w1, a0 = t / (w2 * w1);
-          const float wt = wts[a0 * BIN_CHUNK + i] * wts[(MAXW + a1) * BIN_CHUNK + i] *
-                           wts[(2 * MAXW + a2) * BIN_CHUNK + i];
-          const float2 sv = tile[((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2 + a2];
-          v.x = fmaf(wt, sv.x, v.x);
-          v.y = fmaf(wt, sv.y, v.y);
+#pragma unroll
+        for (int t0 = 0; t0 < NTAPS; t0 += 32) {
+          const int t = t0 + lane;
+          if (NTAPS % 32 == 0 || t < NTAPS) {
+            const int a2 = t % W, a1 = (t / W) % W, a0 = (ND == 3) ? t / (W * W) : 0;
+            const float wt = wts[(a0) * BIN_CHUNK + i] * wts[(W + a1) * BIN_CHUNK + i] *
+                             wts[(2 * W + a2) * BIN_CHUNK + i];
+            const float2 sv = tile[cbase + (a0 * T1 + a1) * T2 + a2];
+            v.x = fmaf(wt, sv.x, v.x);
+            v.y = fmaf(wt, sv.y, v.y);
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -567,6 +579,7 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
       const float wi = wgt ? wgt[sidx] : 1.f;
       if (MODE == 1) {
         if (lane == 0) {
+          const long long oi = orig ? orig[sidx] : sidx;
           float2 yv = cscale(v, wi * scale);
           if (ymeas) {
             yv = csub(yv, ymeas[(long long)j * N + oi]);
@@ -576,27 +589,29 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
         }
         continue;
       }
-      if (MODE == 0) v = cscale(v, wi * scale);
-      else v = cscale(y[(long long)j * N + oi], wi * scale);
-      for (int t = lane; t < ntaps; t += 32) {
-        const int a2 = t % w2, a1 = (t / w2) % w1, a0 = t / (w2 * w1);
-        const float wt = wts[a0 * BIN_CHUNK + i] * wts[(MAXW + a1) * BIN_CHUNK + i] *
-                         wts[(2 * MAXW + a2) * BIN_CHUNK + i];
-        smem_add_f2(&acc[((l0 + a0) * tb[1] + (l1 + a1)) * tb[2] + l2 + a2], cscale(v, wt));
+      if (MODE == 0) {
+        v = cscale(v, wi * scale);
+      } else {
+        const long long oi = orig ? orig[sidx] : sidx;
+        v = cscale(y[(long long)j * N + oi], wi * scale);
+      }
+#pragma unroll
+      for (int t0 = 0; t0 < NTAPS; t0 += 32) {
+        const int t = t0 + lane;
+        if (NTAPS % 32 == 0 || t < NTAPS) {
+          const int a2 = t % W, a1 = (t / W) % W, a0 = (ND == 3) ? t / (W * W) : 0;
+          const float wt = wts[(a0) * BIN_CHUNK + i] * wts[(W + a1) * BIN_CHUNK + i] *
+                           wts[(2 * W + a2) * BIN_CHUNK + i];
+          smem_add_f2(&acc[cbase + (a0 * T1 + a1) * T2 + a2], cscale(v, wt));
+        }
       }
     }
     if (MODE != 1) {
       __syncthreads();
-      for (int e = tid; e < cells; e += BIN_THREADS) {
+      for (int e = tid; e < CELLS; e += BIN_THREADS) {
         const float2 av = acc[e];
         if (av.x == 0.f && av.y == 0.f) continue;
-        const int c2 = e % tb[2];
-        const int c1 = (e / tb[2]) % tb[1];
-        const int c0 = e / (tb[2] * tb[1]);
-        const int k0 = (org[0] + c0) % g.g[0], k1 = (org[1] + c1) % g.g[1], k2 = (org[2] + c2) % g.g[2];
-        const long long off = (long long)perm_of(k0, g.P[0], g.Q[0]) * g.g[1] * g.g[2] +
-                              (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] + perm_of(k2, g.P[2], g.Q[2]);
-        red_add_f2(dst + go + off, av);
+        red_add_f2(dst + go + cell_off(e), av);
       }
     }
   }
@@ -612,31 +627,50 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
   }
 }
 
-size_t bin_smem(const NufftGeom& g, int B, int mode) {
-  long long cells = 1;
-  for (int a = 0; a < 3; ++a) cells *= (g.n[a] > 1) ? (B + g.width - 1) : 1;
-  const long long tiles = (mode == 0) ? 2 : 1;
-  return (size_t)(sizeof(float2) * cells * tiles + sizeof(float) * 3 * MAXW * BIN_CHUNK +
-                  sizeof(short) * 3 * BIN_CHUNK + 16);
+template <int MODE, int ND, int W, int B>
+int launch_bins_t(const float2* src, float2* dst, const int* base, const float* frac, const float* wgt,
+                  const int* orig, long long N, const int* chunks, int nchunks, const NufftGeom& g, int ncoils,
+                  float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
+  using C = BinCfg<ND, W, B>;
+  const size_t smem = sizeof(float2) * C::CELLS * ((MODE == 0) ? 2 : 1) + sizeof(float) * 3 * W * BIN_CHUNK +
+                      sizeof(short) * 3 * BIN_CHUNK + 16;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k_nufft_bins<MODE, ND, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return SR_ECUDA;
+    configured = true;
+  }
+  if (nchunks < 1) return SR_OK;
+  k_nufft_bins<MODE, ND, W, B><<<nchunks, BIN_THREADS, smem, st>>>(src, dst, base, frac, wgt, orig, N, chunks, g,
+                                                                   ncoils, scale, y, ymeas, partial);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
+// binned gridding instantiations: (ND, W, B)
+#define SR_BIN_CFGS(X) X(3, 4, 8) X(3, 4, 4) X(3, 6, 8) X(3, 6, 4) X(2, 4, 16) X(2, 4, 4) X(2, 6, 16) X(2, 6, 4)
+
+bool bins_supported(const NufftGeom& g, int B) {
+  const int nd = (g.n[0] > 1) ? 3 : 2;
+#define X(ND_, W_, B_) if (nd == ND_ && g.width == W_ && B == B_) return true;
+  SR_BIN_CFGS(X)
+#undef X
+  return false;
 }
 
 template <int MODE>
 int launch_bins(const float2* src, float2* dst, const int* base, const float* frac, const float* wgt,
                 const int* orig, long long N, const int* chunks, int nchunks, const NufftGeom& g, int B,
                 int ncoils, float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
-  const size_t smem = bin_smem(g, B, MODE);
-  static size_t configured = 0;
-  if (smem > configured) {
-    if (cudaFuncSetAttribute(k_nufft_bins<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return SR_ECUDA;
-    configured = smem;
-  }
-  if (nchunks < 1) return SR_OK;
-  k_nufft_bins<MODE><<<nchunks, BIN_THREADS, smem, st>>>(src, dst, base, frac, wgt, orig, N, chunks, g, B, ncoils,
-                                                         scale, y, ymeas, partial);
-  SR_CHECK_LAUNCH();
-  return SR_OK;
+  const int nd = (g.n[0] > 1) ? 3 : 2;
+#define X(ND_, W_, B_)                                                                                     \
+  if (nd == ND_ && g.width == W_ && B == B_)                                                              \
+    return launch_bins_t<MODE, ND_, W_, B_>(src, dst, base, frac, wgt, orig, N, chunks, nchunks, g, ncoils, \
+                                           scale, y, ymeas, partial, st);
+  SR_BIN_CFGS(X)
+#undef X
+  return SR_EUNSUPPORTED;
 }
 
 int grid_fft(float2* grid, const NufftGeom& g, int ncoils, int inv, cudaStream_t st) {
@@ -704,7 +738,7 @@ int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, i
   int rc = grid_fft(src, g, ncoils, 0, st);
   if (rc) return rc;
   if (cudaMemsetAsync(dst, 0, sizeof(float2) * ncoils * g.G, st) != cudaSuccess) return SR_ECUDA;
-  if (chunks) {
+  if (chunks && bins_supported(g, binsize)) {
     rc = launch_bins<0>(src, dst, base, frac, wgt, nullptr, nsamples, chunks, nchunks, g, binsize, ncoils,
                         (float)(1.0 / (double)g.D), nullptr, nullptr, nullptr, st);
     if (rc) return rc;
@@ -739,7 +773,7 @@ int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int*
   SR_CHECK_LAUNCH();
   int rc = grid_fft(src, g, ncoils, 0, st);
   if (rc) return rc;
-  if (chunks)
+  if (chunks && bins_supported(g, binsize))
     return launch_bins<1>(src, nullptr, base, frac, sqrtw, orig, nsamples, chunks, nchunks, g, binsize, ncoils,
                           (float)(1.0 / sqrt((double)g.D)), (float2*)y, (const float2*)ymeas, partial, st);
   k_nufft_samples<<<sample_blocks(nsamples), 128, 0, st>>>(1, src, nullptr, base, frac, sqrtw, orig, nsamples,
@@ -760,7 +794,7 @@ int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int*
   cudaStream_t st = (cudaStream_t)stream;
   float2* dst = (float2*)grids;
   if (cudaMemsetAsync(dst, 0, sizeof(float2) * ncoils * g.G, st) != cudaSuccess) return SR_ECUDA;
-  if (chunks) {
+  if (chunks && bins_supported(g, binsize)) {
     int rc0 = launch_bins<2>(nullptr, dst, base, frac, sqrtw, orig, nsamples, chunks, nchunks, g, binsize, ncoils,
                              (float)(1.0 / sqrt((double)g.D)), (float2*)y, nullptr, nullptr, st);
     if (rc0) return rc0;
