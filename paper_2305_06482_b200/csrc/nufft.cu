@@ -503,6 +503,7 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
   float2* acc = tile + ((MODE == 2) ? 0 : CELLS);                         // spread accumulator (0, 2)
   float* wts = reinterpret_cast<float*>(acc + ((MODE == 1) ? 0 : CELLS));  // [3][W][BIN_CHUNK]
   short* loc = reinterpret_cast<short*>(wts + 3 * W * BIN_CHUNK);          // [3][BIN_CHUNK]
+  int* coff = reinterpret_cast<int*>(loc + 3 * BIN_CHUNK + 2);             // [CELLS] grid offsets
   const int* ch = chunks + 5 * blockIdx.x;
   const int org0 = ch[0], org1 = ch[1], org2 = ch[2];
   const int s0 = ch[3], ns = ch[4];
@@ -541,6 +542,7 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
     return (long long)perm_of(k0, g.P[0], g.Q[0]) * sg12 + (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] +
            perm_of(k2, g.P[2], g.Q[2]);
   };
+  for (int e = tid; e < CELLS; e += BIN_THREADS) coff[e] = (int)cell_off(e);  // once per chunk
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARPS = BIN_THREADS / 32;
   double acc2 = 0.0;
@@ -548,7 +550,7 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
     const long long go = (long long)j * g.G;
     __syncthreads();
     for (int e = tid; e < CELLS; e += BIN_THREADS) {
-      if (MODE != 2) tile[e] = src[go + cell_off(e)];
+      if (MODE != 2) tile[e] = src[go + coff[e]];
       if (MODE != 1) acc[e] = make_float2(0.f, 0.f);
     }
     __syncthreads();
@@ -611,7 +613,7 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
       for (int e = tid; e < CELLS; e += BIN_THREADS) {
         const float2 av = acc[e];
         if (av.x == 0.f && av.y == 0.f) continue;
-        red_add_f2(dst + go + cell_off(e), av);
+        red_add_f2(dst + go + coff[e], av);
       }
     }
   }
@@ -633,7 +635,7 @@ int launch_bins_t(const float2* src, float2* dst, const int* base, const float* 
                   float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
   using C = BinCfg<ND, W, B>;
   const size_t smem = sizeof(float2) * C::CELLS * ((MODE == 0) ? 2 : 1) + sizeof(float) * 3 * W * BIN_CHUNK +
-                      sizeof(short) * 3 * BIN_CHUNK + 16;
+                      sizeof(short) * (3 * BIN_CHUNK + 2) + sizeof(int) * C::CELLS + 16;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(k_nufft_bins<MODE, ND, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
