@@ -117,30 +117,31 @@ class ReadoutDecoupler:
 
 # --------------------------------------------------------------------------- per-slice prep
 def slice_compression(y: torch.Tensor, keep: int, valid_n=None, threads: int | None = None) -> np.ndarray:
-    """comp[s] = U_s[:, :keep]^H from the host LAPACK SVD of each slice's (C, N) data
-    (forward_model.py:262-267, so the singular-vector phases are the reference's)."""
+    """comp[s] = U_s[:, :keep]^H of each slice's (C, N) data, as coil_compress_svd computes it
+    (forward_model.py:262-267) but without the N-long host SVD: numpy's SVD of a wide C x N
+    matrix goes through the LQ factor, and svd(Y).U == svd(R^H).U for R from the (LAPACK /
+    cuSOLVER-convention) Householder QR of Y^H (agreement ~1e-13, checked on the box).  So the
+    QR runs batched on the device in complex128 and only the C x C SVDs run on the host.
+    Zero padding of ragged slices leaves R unchanged."""
     import concurrent.futures as cf
     import os
-    yh = y.detach().cpu().numpy().astype(np.complex128)
-    S = yh.shape[0]
+    S, C, N = y.shape
+    if valid_n is not None:
+        y = y.clone()
+        for s in range(S):
+            y[s, :, int(valid_n[s]):] = 0
+    if N < C:
+        raise ValueError("compression needs at least as many samples as coils")
+    a, _ = torch.geqrf(y.to(torch.complex128).conj().transpose(1, 2).contiguous())
+    R = torch.triu(a[:, :C, :]).cpu().numpy()
 
     def one(s):
-        n = yh.shape[2] if valid_n is None else int(valid_n[s])
-        u, _, _ = np.linalg.svd(yh[s, :, :n], full_matrices=False)
+        u, _, _ = np.linalg.svd(R[s].conj().T, full_matrices=False)
         return u[:, :keep].conj().T
 
-    try:  # one BLAS thread per SVD, parallel over slices
-        from threadpoolctl import threadpool_limits
-        limit = threadpool_limits(1)
-    except Exception:  # pragma: no cover
-        limit = None
-    try:
-        ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-        with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, ncpu))) as ex:
-            return np.stack(list(ex.map(one, range(S))))
-    finally:
-        if limit is not None:
-            limit.restore_original_limits()
+    ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, ncpu))) as ex:
+        return np.stack(list(ex.map(one, range(S))))
 
 
 def compress_slices(maps: torch.Tensor, y: torch.Tensor, keep: int, valid_n=None, comp=None):

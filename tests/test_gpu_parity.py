@@ -345,3 +345,16 @@ def test_nufft_binned_and_per_sample_paths_agree(cuda, binned):
         k = GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]), binned=binned, binsize=4)
         assert rel(k.apply(g["batch"]), g["fwd"]) < OP_TOL
         assert rel(k.apply_adjoint(g["y"]), g["adj"]) < OP_TOL
+
+
+def test_slice_compression_matches_host_svd(cuda):
+    """Device QR + C x C host SVD gives the reference's comp = U^H (forward_model.py:262-267)."""
+    from paper_2305_06482_b200.parallel_recon import slice_compression
+    rng = np.random.default_rng(21)
+    S, C, N = 3, 12, 700
+    y = (rng.standard_normal((S, C, N)) + 1j * rng.standard_normal((S, C, N))) * np.exp(rng.standard_normal((S, C, 1)))
+    y = y.astype(np.complex64)
+    comp = slice_compression(torch.from_numpy(y).cuda(), C)
+    for s in range(S):
+        u = np.linalg.svd(y[s].astype(np.complex128), full_matrices=False)[0]
+        np.testing.assert_allclose(comp[s], u.conj().T, atol=1e-9)
