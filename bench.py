@@ -333,6 +333,13 @@ def main():
     ms = t_s / args.steps * 1e3
     bytes_apply = algorithmic_bytes()
     peak, peak_kind = measured_peak()
+    traffic = None
+    tp = ROOT / "profiles" / "k1_traffic.json"
+    if tp.exists():
+        try:
+            traffic = float(json.loads(tp.read_text())["traffic_bytes"])
+        except Exception:
+            traffic = None
     achieved = bytes_apply / (t_s / args.steps) / 1e9
     if rank == 0:
         cpu = None if args.no_cpu_baseline else cpu_baseline_single(args.seed)
@@ -352,7 +359,9 @@ def main():
             "unsketched_32coil": {"value": world * max(3, args.steps // 5) / t_full, "unit": UNIT,
                                   "speedup_sketched": (world * args.steps / t_s) / (world * max(3, args.steps // 5) / t_full)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per apply "
+                                           "(profiles/k1_traffic.json)",
                          "kernel": "K1 fused sketched normal op (rowfwd + colpass + rowinv launches)",
                          "algorithmic_bytes_per_apply": bytes_apply},
             "gpu_launches": 3 * args.steps,
