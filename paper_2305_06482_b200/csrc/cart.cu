@@ -40,7 +40,7 @@ struct RowCfg {
   static constexpr int ROWS0 = BASE * ((128 / (BASE * P)) > 1 ? (128 / (BASE * P)) : 1);
   static constexpr int ROWS = ROWS0 > 64 ? 64 : ROWS0;
   static constexpr int T = ROWS * P;
-  static constexpr int MINB = (T <= 128) ? 4 : 3;
+  static constexpr int MINB = (T <= 160) ? 4 : 3;
   static constexpr int MINB_INV = (T <= 128) ? 4 : 3;
   static constexpr int N = P * Q;
   static constexpr int XS = N + ((((P % 16) - (N % 16)) % 16 + 16) % 16);  // x row stride = P (mod 16)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--fused", default="", help="semicolon list of lagB,lagC,slots,tile configs of the persistent launch")
     ap.add_argument("--stats", action="store_true", help="collect fused-kernel wait/item statistics")
+    ap.add_argument("--multistream", default="", help="semicolon list of chunk,streams for the three-pass schedule")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     w = bench.build_workload(0, dev)
@@ -45,11 +46,40 @@ def main():
             _lib.call("sr_fused_stats", None)
             rec["stats"] = st.cpu().tolist()
         print(json.dumps(rec), flush=True)
+    for cfg in [c for c in args.multistream.split(";") if c]:
+        ch, ns = (int(v) for v in cfg.split(","))
+        ms = multistream(kern, smaps, x, out, ch, ns)
+        print(json.dumps({"multistream": cfg, "ms_per_apply": ms}), flush=True)
     for ch in [int(c) for c in args.chunks.split(",") if c]:
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=ch), args.steps, 3, torch.cuda.synchronize)
         ms = t / args.steps * 1e3
         print(json.dumps({"chunk": ch, "ms_per_apply": ms,
                           "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}), flush=True)
+
+
+
+
+
+def multistream(kern, smaps, x, out, chunk, nstreams, steps=20):
+    """Three-pass K1 over slice chunks spread round-robin over `nstreams` streams (L2 experiment)."""
+    import torch
+    ncoils = smaps.shape[1]
+    B = kern.batch
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    wss = [torch.empty(chunk * ncoils * kern.D, dtype=torch.complex64, device=x.device) for _ in range(nstreams)]
+    cur = torch.cuda.current_stream()
+
+    def once():
+        for s in streams:
+            s.wait_stream(cur)
+        for i, b0 in enumerate(range(0, B, chunk)):
+            k = i % nstreams
+            kern._normal_range(smaps, x, out, b0, min(B, b0 + chunk), wss[k], streams[k].cuda_stream)
+        for s in streams:
+            cur.wait_stream(s)
+
+    t = bench.time_applies(once, steps, 3, torch.cuda.synchronize)
+    return t / steps * 1e3
 
 
 if __name__ == "__main__":
