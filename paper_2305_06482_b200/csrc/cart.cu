@@ -53,7 +53,7 @@ template <int P, int Q>
 __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          const float2* __restrict__ maps, float2* __restrict__ ws,
-         int ncoils, int ny, long long x_bstride, long long map_bstride, int tws) {
+         int ncoils, int ny, long long x_bstride, long long map_bstride) {
   using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   constexpr int XS = RowCfg<P, Q>::XS;
@@ -117,15 +117,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
       __syncthreads();
     }
     float2* wj = wb + j * D;
-    if (tws) {
-      // transposed workspace [pos_x][y]: lanes over the CTA's rows -> 8-row (64 B) segments
-      float2* wt = ws + ((long long)b * ncoils + j) * D + row0;
-      const int nr = min(ROWS, ny - row0);
-      for (int e = tid; e < ROWS * N; e += T) {
-        const int r = e % ROWS, pos = e / ROWS;
-        if (r < nr) wt[(long long)pos * ny + r] = buf[r * S::VS + S::pad(pos)];
-      }
-    } else if constexpr (S::VEC) {
+    if constexpr (S::VEC) {
       for (int e = 2 * tid; e < nvalid; e += 2 * T) {
         const int l3 = e / N, pos = e - l3 * N;
         *reinterpret_cast<float4*>(wj + e) = *reinterpret_cast<const float4*>(buf + l3 * S::VS + S::pad(pos));
@@ -148,7 +140,7 @@ __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB_INV)
 k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
-         const float2* __restrict__ u, const float2* __restrict__ d, float oscale, int tws) {
+         const float2* __restrict__ u, const float2* __restrict__ d, float oscale) {
   using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   extern __shared__ __align__(16) float2 dsm[];
@@ -171,14 +163,7 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   auto issue_tile = [&](int j) {
     const float2* wj = wb + j * D;
     float2* dst = bufs + (j & 1) * (ROWS * S::VS);
-    if (tws) {
-      const float2* wt = ws + ((long long)b * ncoils + j) * D + row0;
-      const int nr = min(ROWS, ny - row0);
-      for (int e = tid; e < ROWS * N; e += T) {
-        const int r = e % ROWS, pos = e / ROWS;
-        if (r < nr) cp_async8(dst + r * S::VS + S::pad(pos), wt + (long long)pos * ny + r);
-      }
-    } else if constexpr (S::VEC) {
+    if constexpr (S::VEC) {
       for (int e = 2 * tid; e < nvalid; e += 2 * T) {
         const int l3 = e / N, pos = e - l3 * N;
         cp_async16(dst + l3 * S::VS + S::pad(pos), wj + e);
@@ -351,101 +336,6 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
   }
 }
 
-// --------------------------------------------------- pass B on the transposed workspace
-// The normal op keeps the coil workspace transposed ([pos_x][y]) between the passes, so
-// the column FFT . mask . IFFT runs on contiguous vectors with the row-pass machinery
-// (coalesced LDG/STG over p, 128-bit shared group moves); the mask row of a vector is
-// maskT[pos_x][:] (contiguous).  One (slice, coil), ROWS vectors per CTA, in place.
-template <int P, int Q>
-__global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
-k_colrows(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long mask_bstride, int nvec,
-          int ncoils) {
-  using S = RowShape<P, Q>;
-  constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
-  extern __shared__ __align__(16) float2 dsm[];
-  float2* t1 = dsm;
-  float2* t2 = dsm + N;
-  float2* buf = dsm + 2 * N;
-  const int tid = threadIdx.x;
-  const int v0 = blockIdx.x * ROWS;
-  const int j = blockIdx.y, b = blockIdx.z;
-  const int lr = tid / P, p = tid % P;
-  const int vec = v0 + lr;
-  const bool valid = vec < nvec;
-  init_tw_s1<P, Q>(t1, tid, T);
-  init_tw_s2<P, Q>(t2, tid, T);
-  __syncthreads();
-  float2* img = ws + ((long long)b * ncoils + j) * ((long long)nvec * N);
-  float2* vr = img + (long long)vec * N + p;
-  float2 r[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) r[q] = valid ? vr[P * q] : make_float2(0.f, 0.f);
-  fft_s1_fwd<P, Q>(r, p, t1);
-#pragma unroll
-  for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
-  __syncthreads();
-  const uint8_t* mrow = maskT + b * mask_bstride;
-  for (int it = tid; it < ROWS * Q; it += T) {
-    const int l2 = it / Q, k2 = it - l2 * Q;
-    if (v0 + l2 >= nvec) continue;
-    float2 g[P];
-    float2* gp = buf + l2 * S::VS + S::GS * k2;
-    lds_group<P, S::VEC>(g, gp);
-    if (P > 1) fft_s2_fwd<P>(g);
-    const uint8_t* mk = mrow + (long long)(v0 + l2) * N + P * k2;
-    if constexpr (P % 4 == 0) {
-#pragma unroll
-      for (int w4 = 0; w4 < P / 4; ++w4) {
-        const uint32_t m4 = __ldg(reinterpret_cast<const uint32_t*>(mk) + w4);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) g[4 * w4 + i] = ((m4 >> (8 * i)) & 0xffu) ? g[4 * w4 + i] : make_float2(0.f, 0.f);
-      }
-    } else {
-#pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = mk[k1] ? g[k1] : make_float2(0.f, 0.f);
-    }
-    if (P > 1) fft_s2_inv<P, Q>(g, k2, t2);
-    sts_group<P, S::VEC>(gp, g);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[lr * S::VS + S::GS * k2 + p];
-  fft_s1_inv<Q>(r);
-  if (valid) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) vr[P * q] = r[q];
-  }
-}
-
-template <int P, int Q>
-int launch_colrows(float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, int nvec,
-                   cudaStream_t st) {
-  using R = RowCfg<P, Q>;
-  const size_t smem = sizeof(float2) * (2 * P * Q + R::ROWS * RowShape<P, Q>::VS);
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(k_colrows<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return SR_ECUDA;
-    configured = true;
-  }
-  dim3 grid((nvec + R::ROWS - 1) / R::ROWS, ncoils, batch);
-  k_colrows<P, Q><<<grid, R::T, smem, st>>>(ws, maskT, mbs, nvec, ncoils);
-  SR_CHECK_LAUNCH();
-  return SR_OK;
-}
-
-int dispatch_colrows(int ny, float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, int nx,
-                     cudaStream_t st) {
-  switch (ny) {
-#define X(N, P, Q) \
-  case N: return launch_colrows<P, Q>(ws, maskT, mbs, batch, ncoils, nx, st);
-    SR_FFT_SIZES(X)
-#undef X
-    default: return SR_EUNSUPPORTED;
-  }
-}
-
 // ------------------------------------------------------------- gather/scatter
 // y[b, j, i] = scale * ph[i] * spec[b, j, spos[i]]  (- ymeas[b, j, i])
 // ragged samples: slice b owns [soff[b], soff[b+1]) of spos/ph; y rows are
@@ -504,7 +394,7 @@ __global__ void k_scatter(float2* __restrict__ ws, const int* __restrict__ spos,
 // ---------------------------------------------------------------- dispatch
 template <int P, int Q>
 int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, float2* ws,
-                  int batch, int ncoils, int ny, long long xbs, long long mbs, int tws, cudaStream_t st) {
+                  int batch, int ncoils, int ny, long long xbs, long long mbs, cudaStream_t st) {
   using R = RowCfg<P, Q>;
   static bool configured = false;
   if (!configured) {
@@ -514,7 +404,7 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
     configured = true;
   }
   dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
-  k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs, tws);
+  k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -522,7 +412,7 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
 template <int P, int Q>
 int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, int ncoils,
                   int ny, long long xbs, long long mbs, const float4* coef, const float2* u,
-                  const float2* d, float oscale, int tws, cudaStream_t st) {
+                  const float2* d, float oscale, cudaStream_t st) {
   using R = RowCfg<P, Q>;
   static bool configured = false;
   if (!configured) {
@@ -532,7 +422,7 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
     configured = true;
   }
   dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
-  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d, oscale, tws);
+  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d, oscale);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -557,10 +447,10 @@ int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale
 
 int dispatch_rowfwd(int nx, const float2* x, const float2* anchor, const float2* maps,
                     float2* ws, int batch, int ncoils, int ny, long long xbs, long long mbs,
-                    cudaStream_t st, int tws = 0) {
+                    cudaStream_t st) {
   switch (nx) {
 #define X(N, P, Q) \
-  case N: return launch_rowfwd<P, Q>(x, anchor, maps, ws, batch, ncoils, ny, xbs, mbs, tws, st);
+  case N: return launch_rowfwd<P, Q>(x, anchor, maps, ws, batch, ncoils, ny, xbs, mbs, st);
     SR_FFT_SIZES(X)
 #undef X
     default: return SR_EUNSUPPORTED;
@@ -569,12 +459,12 @@ int dispatch_rowfwd(int nx, const float2* x, const float2* anchor, const float2*
 
 int dispatch_rowinv(int nx, const float2* ws, const float2* maps, float2* out, int batch,
                     int ncoils, int ny, long long xbs, long long mbs, const float4* coef,
-                    const float2* u, const float2* d, float oscale, cudaStream_t st, int tws = 0) {
+                    const float2* u, const float2* d, float oscale, cudaStream_t st) {
   switch (nx) {
 #define X(N, P, Q)                                                                      \
   case N:                                                                               \
     return launch_rowinv<P, Q>(ws, maps, out, batch, ncoils, ny, xbs, mbs, coef, u, d, \
-                               oscale, tws, st);
+                               oscale, st);
     SR_FFT_SIZES(X)
 #undef X
     default: return SR_EUNSUPPORTED;
@@ -655,13 +545,12 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
     const float4* cc = coef ? (const float4*)coef + b0 : nullptr;
     const float2* uc = u ? (const float2*)u + xo : nullptr;
     const float2* dc = d ? (const float2*)d + xo : nullptr;
-    // transposed coil workspace between the passes (column pass on contiguous vectors)
-    int rc = dispatch_rowfwd(nx, xc, ac, mc, (float2*)ws, nb, ncoils, ny, D, map_bstride, st, 1);
+    int rc = dispatch_rowfwd(nx, xc, ac, mc, (float2*)ws, nb, ncoils, ny, D, map_bstride, st);
     if (rc) return rc;
-    rc = dispatch_colrows(ny, (float2*)ws, kc, mask_bstride, nb, ncoils, nx, st);
+    rc = dispatch_colpass(ny, (float2*)ws, kc, mask_bstride, 1.f, COL_NORMAL, nb, ncoils, nx, st);
     if (rc) return rc;
     rc = dispatch_rowinv(nx, (const float2*)ws, mc, oc, nb, ncoils, ny, D, map_bstride, cc, uc, dc,
-                         (float)(1.0 / (double)D), st, 1);
+                         (float)(1.0 / (double)D), st);
     if (rc) return rc;
   }
   return SR_OK;
