@@ -56,7 +56,7 @@ class SketchedReconEngine:
     def __init__(self, kernel, maps0: torch.Tensor, y: torch.Tensor, *, dims, sketch: SketchConfig,
                  lam: float, reg: str = "l1-wavelet", solver: str = "fista", step_scale: float = 0.9,
                  sqrt_w: torch.Tensor | None = None, wavelet_levels: int | None = None,
-                 counter: CostCounter | None = None, shard=None):
+                 counter: CostCounter | None = None, shard=None, use_graph: bool = True):
         self.kernel = kernel
         self.maps0 = maps0.contiguous()          # (B, C0, D) all compressed coils (sketch input)
         self.B, self.C0, self.D = self.maps0.shape
@@ -93,6 +93,11 @@ class SketchedReconEngine:
         self.partial = torch.zeros(kernel.partial_shape(max(1, self.maps_full.shape[1])), dtype=torch.float64,
                                    device=self.dev)
         self.tmp = mk() if self.shard is not None else None
+        # the inner FISTA loop of every outer iteration launches the same kernels on the same
+        # buffers, so it is captured once as a CUDA graph and replayed (t >= 2)
+        self.use_graph = bool(use_graph) and self.shard is None
+        self._graph = None
+        self._smaps_buf = None
         self.step = None       # (B,) float64 device
         self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
         self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
@@ -198,6 +203,23 @@ class SketchedReconEngine:
                 self.x.copy_(self.v)
             t_k = t_next
 
+    def _fista_graphed(self, smaps, inner: int):
+        """Replay of the captured inner loop on a persistent sketched-maps buffer."""
+        if self._graph is None:
+            self._smaps_buf = smaps.clone()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            counts = self.counter.asdict()
+            with self.counter.paused():
+                with torch.cuda.graph(g):
+                    self._fista(self._smaps_buf, inner)
+            self.counter._counts = counts
+            self._graph = g
+        else:
+            self._smaps_buf.copy_(smaps)
+        self._graph.replay()
+        self.counter.add("coil_transform", 2 * self.chat * inner)
+
     def _cg(self, smaps, inner: int):
         """(A_s^H A_s + lam I) delta = -d - lam x^t, x = x^t + delta (coil_sketch.py:182-191)."""
         B, D, st = self.B, self.D, dv.stream()
@@ -268,7 +290,10 @@ class SketchedReconEngine:
                     self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
             self.anchor.copy_(self.x)
             if self.solver == "fista":
-                self._fista(smaps, inner)
+                if self.use_graph and t >= 2 and self.reg == "l1-wavelet":
+                    self._fista_graphed(smaps, inner)
+                else:
+                    self._fista(smaps, inner)
             else:
                 self._cg(smaps, inner)
             finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1).cpu().numpy()
