@@ -17,7 +17,7 @@ import torch
 
 from . import _device as dv
 from .forward_model import (DensityWeights, KSpaceData, SenseOperator, SensitivityMaps, build_sense,
-                            coil_compress_svd)
+                            coil_compress_device, coil_compress_svd)
 from .linops import Image, make_fourier_kernel
 from .recon import DIVERGENCE_FACTOR, SketchedReconEngine
 from .rng import child_seed
@@ -151,9 +151,12 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     if not cfg.reuse_step_size:
         raise NotImplementedError("reuse_step_size=False is not implemented on the device path")
     kind = _reg_kind(cfg.reg)
-    data0, maps0, _, energy = coil_compress_svd(data, maps, cfg.c_hat0)
-    a = SenseOperator(maps0, data0.traj, weights, method=method, kernel=kernel)
-    y = dv.c64(a.measurement_vector(data0)).view(1, cfg.c_hat0, a.n_points)
+    maps0_dev, data0_dev, _, energy = coil_compress_device(data, maps, cfg.c_hat0)
+    a = SenseOperator(maps0_dev, data.traj, weights, method=method, kernel=kernel, shape=maps.shape)
+    y = data0_dev
+    if weights is not None and not data.weights_applied:
+        y = y * a.sqrt_w_dev.to(torch.complex64)
+    y = y.view(1, cfg.c_hat0, a.n_points)
     solver_cfg = solver_cfg or SolverConfig(tol=0.0)
     if solver_cfg.tol != 0.0:
         raise NotImplementedError("the device engine runs the fixed-count inner loop (tol = 0)")
@@ -166,7 +169,7 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     if cfg.use_init:
         before = a.counts.get("coil_transform", 0)
         sk0 = gen_sketch_matrix(cfg.sketch.with_seed(child_seed(cfg.sketch.seed, 0)), cfg.c_hat0)
-        x0_dev = dv.c64(classical_sketch_solve(a, a.measurement_vector(data0), sk0, cfg.reg, solver_cfg,
+        x0_dev = dv.c64(classical_sketch_solve(a, dv.to_numpy128(y.reshape(-1)), sk0, cfg.reg, solver_cfg,
                                                cfg.solver).values).view(1, -1)
         init_count = a.counts.get("coil_transform", 0) - before
     eng = SketchedReconEngine(a.kernel, a.maps_dev, ypad, dims=maps.shape.dims, sketch=cfg.sketch,

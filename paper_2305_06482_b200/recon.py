@@ -50,13 +50,32 @@ class EngineResult:
     per_outer_dist: list = field(default_factory=list)
 
 
+_POWER_V0: dict = {}
+GRAPH_MIN_REPLAYED = 400
+
+
+def _power_start(seed: int, d: int, dev) -> torch.Tensor:
+    """Unit start vector of the power iteration (linops.py:766-782), cached per (seed, D, device):
+    generating 2 D normals on the host dominates small-slice setup otherwise."""
+    key = (int(seed), int(d), str(dev))
+    v = _POWER_V0.get(key)
+    if v is None:
+        g = seed_stream(seed, 0)
+        v0 = g.standard_normal(d) + 1j * g.standard_normal(d)
+        v = dv.c64(v0 / np.linalg.norm(v0)).view(1, d).to(dev)
+        if len(_POWER_V0) > 16:
+            _POWER_V0.clear()
+        _POWER_V0[key] = v
+    return v
+
+
 class SketchedReconEngine:
     """Device state of B slices sharing one grid, one Fourier kernel and one sketch design."""
 
     def __init__(self, kernel, maps0: torch.Tensor, y: torch.Tensor, *, dims, sketch: SketchConfig,
                  lam: float, reg: str = "l1-wavelet", solver: str = "fista", step_scale: float = 0.9,
                  sqrt_w: torch.Tensor | None = None, wavelet_levels: int | None = None,
-                 counter: CostCounter | None = None, shard=None, use_graph: bool = True):
+                 counter: CostCounter | None = None, shard=None, use_graph: bool | None = None):
         self.kernel = kernel
         self.maps0 = maps0.contiguous()          # (B, C0, D) all compressed coils (sketch input)
         self.B, self.C0, self.D = self.maps0.shape
@@ -94,8 +113,12 @@ class SketchedReconEngine:
                                    device=self.dev)
         self.tmp = mk() if self.shard is not None else None
         # the inner FISTA loop of every outer iteration launches the same kernels on the same
-        # buffers, so it is captured once as a CUDA graph and replayed (t >= 2)
-        self.use_graph = bool(use_graph) and self.shard is None
+        # buffers, so it can be captured once as a CUDA graph and replayed (t >= 2).  Capture +
+        # instantiation costs ~10 ms, saving ~50 us per inner iteration of launch overhead, so
+        # None (auto) captures only when at least GRAPH_MIN_REPLAYED inner iterations replay.
+        self.use_graph = use_graph if use_graph is None else bool(use_graph)
+        if self.shard is not None:
+            self.use_graph = False
         self._graph = None
         self._smaps_buf = None
         self.step = None       # (B,) float64 device
@@ -157,10 +180,7 @@ class SketchedReconEngine:
 
     def power_lambda(self, smaps, iters: int = 30, seed: int = 0) -> torch.Tensor:
         """lambda_max(A_s^H A_s) per slice (linops.py:766-782), counters paused."""
-        g = seed_stream(seed, 0)
-        v0 = g.standard_normal(self.D) + 1j * g.standard_normal(self.D)
-        v0 = v0 / np.linalg.norm(v0)
-        v = dv.c64(np.broadcast_to(v0, (self.B, self.D)))
+        v = _power_start(seed, self.D, self.dev).repeat(self.B, 1)  # a copy: v is updated in place
         w = torch.empty_like(v)
         nparts = _lib.lib().sr_reduce_nparts()
         part = torch.empty(self.B, nparts, 2, dtype=torch.float64, device=self.dev)
@@ -207,13 +227,15 @@ class SketchedReconEngine:
         """Replay of the captured inner loop on a persistent sketched-maps buffer."""
         if self._graph is None:
             self._smaps_buf = smaps.clone()
-            torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            counts = self.counter.asdict()
-            with self.counter.paused():
-                with torch.cuda.graph(g):
-                    self._fista(self._smaps_buf, inner)
-            self.counter._counts = counts
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side), self.counter.paused():
+                # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
+                g.capture_begin()
+                self._fista(self._smaps_buf, inner)
+                g.capture_end()
+            torch.cuda.current_stream().wait_stream(side)
             self._graph = g
         else:
             self._smaps_buf.copy_(smaps)
@@ -290,7 +312,10 @@ class SketchedReconEngine:
                     self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
             self.anchor.copy_(self.x)
             if self.solver == "fista":
-                if self.use_graph and t >= 2 and self.reg == "l1-wavelet":
+                graph = self.use_graph
+                if graph is None:
+                    graph = (outer - 2) * inner >= GRAPH_MIN_REPLAYED
+                if graph and t >= 2 and self.reg == "l1-wavelet":
                     self._fista_graphed(smaps, inner)
                 else:
                     self._fista(smaps, inner)

@@ -358,3 +358,47 @@ def test_slice_compression_matches_host_svd(cuda):
     for s in range(S):
         u = np.linalg.svd(y[s].astype(np.complex128), full_matrices=False)[0]
         np.testing.assert_allclose(comp[s], u.conj().T, atol=1e-9)
+
+
+def test_coil_compress_device_matches_host(cuda):
+    """Device compression (QR of Y^H + C x C SVD, complex128 rotations) == host coil_compress_svd."""
+    _, fm, lo, _, _ = _api()
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200 import _device as dv
+    rng = np.random.default_rng(5)
+    dims, C, keep = (24, 20), 10, 6
+    pts = synth.mask_points(synth.vd_poisson_mask(dims, 2.5, 6, 1))
+    traj = lo.Trajectory(pts, "cartesian-mask")
+    data = fm.KSpaceData(traj, rng.standard_normal((C, len(pts))) + 1j * rng.standard_normal((C, len(pts))))
+    maps = fm.SensitivityMaps(lo.GridShape(dims), synth.gaussian_coil_maps(dims, C, rng))
+    d0, m0, comp, energy = fm.coil_compress_svd(data, maps, keep)
+    m0d, d0d, comp_d, energy_d = fm.coil_compress_device(data, maps, keep)
+    np.testing.assert_allclose(comp_d, comp, atol=1e-9)
+    assert abs(energy - energy_d) < 1e-12
+    assert rel(dv.to_numpy128(m0d), m0.coils) < 1e-6
+    assert rel(dv.to_numpy128(d0d), d0.coils) < 1e-6
+
+
+def test_graphed_inner_loop_matches_eager(cuda):
+    """The CUDA-graph replay of the inner FISTA loop launches the same kernels on the same buffers:
+    its iterates are bitwise those of the eager loop."""
+    cs, fm, lo, sk, so = _api()
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    from paper_2305_06482_b200.recon import SketchedReconEngine
+    rng = np.random.default_rng(13)
+    C, dims = 8, (48, 40)
+    pts = synth.mask_points(synth.vd_poisson_mask(dims, 3.0, 8, 2))
+    maps = torch.from_numpy(synth.gaussian_coil_maps(dims, C, rng).astype(np.complex64)).cuda().view(1, C, -1)
+    kern = CartesianKernel(dims, [cartesian_plan(dims, pts)], batch=1)
+    y = torch.zeros(1, C, kern.nmax, dtype=torch.complex64, device="cuda")
+    y[:, :, : len(pts)] = torch.from_numpy(
+        (rng.standard_normal((C, len(pts))) + 1j * rng.standard_normal((C, len(pts)))).astype(np.complex64)).cuda()
+    res = []
+    for graph in (False, True):
+        eng = SketchedReconEngine(kern, maps, y, dims=dims, sketch=sk.SketchConfig(4, 2, 2), lam=1e-3,
+                                  reg="l1-wavelet", solver="fista", use_graph=graph)
+        res.append(eng.run(4, 5))
+    assert torch.equal(res[0].x, res[1].x)
+    np.testing.assert_array_equal(np.asarray(res[0].objectives), np.asarray(res[1].objectives))
