@@ -64,6 +64,16 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk,
                    void* stream);
 
+/* chunk == -2 (group schedule, cart_group.cu): one persistent launch in which groups of
+ * G co-resident CTAs share each coil image through an L2-resident scratch image, so the
+ * coil workspace never streams through HBM.  Instantiated for the (ny, nx) pairs below
+ * report 1 from sr_group_normal_supported; sr_group_ngroups is the number of CTA groups
+ * the current device runs concurrently (0 if unsupported). */
+int sr_group_normal_supported(int ny, int nx);
+int sr_group_ngroups(int ny, int nx);
+/* Tuning: prefer group size g where an instantiation exists (0 = each size's default). */
+int sr_group_select(int g);
+
 /* Workspace bytes sr_cart_normal needs for these arguments. */
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
 /* 1 if the persistent fused K1 is instantiated for an ny x nx grid. */

@@ -39,6 +39,9 @@ SIGNATURES = {
     "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
     "sr_fused_normal_supported": [_i, _i],
+    "sr_group_normal_supported": [_i, _i],
+    "sr_group_ngroups": [_i, _i],
+    "sr_group_select": [_i],
     "sr_fused_config": [_i, _i, _i, _i],
     "sr_fused_stats": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,

@@ -27,6 +27,13 @@ int sr_fused_normal(const float2* x, const float2* anchor, const float2* maps, l
                     int batch, int ncoils, int ny, int nx, const float4* coef, const float2* u,
                     const float2* d, cudaStream_t st);
 
+// cart_group.cu
+long long sr_group_ws_bytes(int batch, int ny, int nx);
+int sr_group_normal(const float2* x, const float2* anchor, const float2* maps, long long map_bstride,
+                    const uint8_t* maskT, long long mask_bstride, float2* out, void* ws, int batch,
+                    int ncoils, int ny, int nx, const float4* coef, const float2* u, const float2* d,
+                    cudaStream_t st);
+
 namespace {
 
 // ------------------------------------------------------------------- pass A
@@ -511,6 +518,7 @@ int sr_fft_split(int n, int* P, int* Q) {
 
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk) {
   const long long D = (long long)ny * nx;
+  if (chunk == -2 && sr_group_normal_supported(ny, nx)) return sr_group_ws_bytes(batch, ny, nx);
   if (chunk == -1 && sr_fused_normal_supported(ny, nx))
     return 8LL * sr_fused_ws_elems(batch, ncoils, D) + 4LL * sr_fused_sync_ints(batch, ncoils, ny) + 256;
   const int nb = (chunk <= 0 || chunk > batch) ? batch : chunk;
@@ -521,8 +529,14 @@ int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk, void* stream) {
-  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < -1) return SR_EINVAL;
+  if (batch < 1 || ncoils < 1 || ny < 1 || nx < 2 || chunk < -2) return SR_EINVAL;
   if (!fft_size_supported(nx) || !fft_size_supported(ny)) return SR_EUNSUPPORTED;
+  if (chunk == -2) {
+    if (!sr_group_normal_supported(ny, nx)) return SR_EUNSUPPORTED;
+    return sr_group_normal((const float2*)x, (const float2*)anchor, (const float2*)maps, map_bstride,
+                           maskT, mask_bstride, (float2*)out, ws, batch, ncoils, ny, nx,
+                           (const float4*)coef, (const float2*)u, (const float2*)d, (cudaStream_t)stream);
+  }
   if (chunk == -1) {
     if (!sr_fused_normal_supported(ny, nx)) return SR_EUNSUPPORTED;
     const long long D = (long long)ny * nx;

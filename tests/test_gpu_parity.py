@@ -80,7 +80,7 @@ def test_wavelet_and_prox(cuda, name):
     assert abs(reg.value(g["x"]) - float(g["value"])) < 1e-5 * float(g["value"])
 
 
-@pytest.mark.parametrize("dims", [(320, 320), (256, 256), (256, 160), (64, 40), (200, 80)])
+@pytest.mark.parametrize("dims", [(320, 320), (256, 256), (256, 160), (64, 64), (64, 40), (200, 80)])
 def test_batched_normal_op_vs_oracle(cuda, dims):
     """K1 at BASELINE geometries (a few slices, per-slice masks and maps)."""
     from paper_2305_06482_b200.cartesian import CartesianKernel
@@ -108,6 +108,7 @@ def test_batched_normal_op_vs_oracle(cuda, dims):
     # the other schedules of the same operator: chunked three-pass and the persistent launch
     from paper_2305_06482_b200 import _lib
     schedules = [2] + ([-1] if _lib.lib().sr_fused_normal_supported(*dims) else [])
+    schedules += [-2] if _lib.lib().sr_group_normal_supported(*dims) else []
     for ch in schedules:
         out2 = torch.full_like(xd, float("nan"))
         kern.normal(md, xd, out2, chunk=ch)
@@ -126,6 +127,37 @@ def test_batched_normal_op_vs_oracle(cuda, dims):
         a = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b]))
         n = len(pts_all[b])
         assert rel(adj[b].cpu().numpy(), a.adjoint(y[b, :, :n].cpu().numpy().astype(np.complex128).ravel())) < OP_TOL
+
+
+@pytest.mark.parametrize("dims,B,C", [((320, 320), 4, 12), ((64, 64), 3, 5), ((256, 160), 2, 7)])
+def test_group_schedule_epilogue_and_determinism(cuda, dims, B, C):
+    """Group schedule (chunk -2): anchor + FISTA epilogue equal to the three-pass schedule,
+    slices split across CTA groups (partials combined in group order), bitwise repeatable."""
+    from paper_2305_06482_b200 import _lib
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    if not _lib.lib().sr_group_normal_supported(*dims):
+        pytest.skip("size not instantiated")
+    rng = np.random.default_rng(11)
+    D = dims[0] * dims[1]
+    plans = []
+    for b in range(B):
+        pts = np.argwhere(rng.random(dims) < 0.25) - np.array([n // 2 for n in dims])
+        plans.append(cartesian_plan(dims, pts))
+    kern = CartesianKernel(dims, plans)
+    t = lambda v: torch.from_numpy(v.astype(np.complex64)).cuda()  # noqa: E731
+    cplx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
+    maps = t(cplx(B, C, D) / 3)
+    z, a, d = t(cplx(B, D)), t(cplx(B, D)), t(cplx(B, D))
+    coef = torch.tensor([[-0.3 - 0.1 * b, 1.0, -0.2, 0.0] for b in range(B)], dtype=torch.float32,
+                        device="cuda")
+    outs = []
+    for ch in (0, -2, -2):
+        o = torch.full_like(z, float("nan"))
+        kern.normal(maps, z, o, anchor=a, coef=coef, u=z, d=d, chunk=ch)
+        outs.append(o.cpu().numpy())
+    assert rel(outs[1], outs[0]) < 1e-5
+    np.testing.assert_array_equal(outs[1], outs[2])
 
 
 def test_fused_fista_epilogue(cuda):

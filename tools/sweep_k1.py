@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--chunks", default="0,32,16")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--fused", default="", help="semicolon list of lagB,lagC,slots,tile configs of the persistent launch")
+    ap.add_argument("--group", default="", help="comma list of group sizes G for chunk -2")
     ap.add_argument("--stats", action="store_true", help="collect fused-kernel wait/item statistics")
     ap.add_argument("--multistream", default="", help="semicolon list of chunk,streams for the three-pass schedule")
     args = ap.parse_args()
@@ -50,6 +51,13 @@ def main():
         ch, ns = (int(v) for v in cfg.split(","))
         ms = multistream(kern, smaps, x, out, ch, ns)
         print(json.dumps({"multistream": cfg, "ms_per_apply": ms}), flush=True)
+    for g in [int(c) for c in args.group.split(",") if c]:
+        _lib.call("sr_group_select", g)
+        t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=-2), args.steps, 3, torch.cuda.synchronize)
+        ms = t / args.steps * 1e3
+        print(json.dumps({"group": g, "ngroups": _lib.lib().sr_group_ngroups(kern.ny, kern.nx), "ms_per_apply": ms,
+                          "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}), flush=True)
+    _lib.call("sr_group_select", 0)
     for ch in [int(c) for c in args.chunks.split(",") if c]:
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=ch), args.steps, 3, torch.cuda.synchronize)
         ms = t / args.steps * 1e3
