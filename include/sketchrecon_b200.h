@@ -74,6 +74,10 @@ int sr_group_ngroups(int ny, int nx);
 /* Tuning: prefer group size g where an instantiation exists (0 = each size's default). */
 int sr_group_select(int g);
 
+/* Tuning of the three-launch schedule: coils per CTA of the column pass (0 = one coil per
+ * CTA, the generic kernel; default 4). */
+int sr_cart_tune(int col_jc);
+
 /* Workspace bytes sr_cart_normal needs for these arguments. */
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
 /* 1 if the persistent fused K1 is instantiated for an ny x nx grid. */

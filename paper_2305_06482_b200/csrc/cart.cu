@@ -77,28 +77,40 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   const long long D = (long long)ny * N;
   const int nvalid = min(ROWS, ny - row0) * N;
   init_tw_s1<P, Q>(t1, tid, T);
-  // stage u = x - anchor for the CTA's rows once; reused by every coil
-  {
-    const float2* xb = x + b * x_bstride + (long long)row0 * N;
-    const float2* ab = anchor ? anchor + b * x_bstride + (long long)row0 * N : nullptr;
-    for (int e = tid; e < ROWS * N; e += T) {
-      const int l3 = e / N, pos = e - l3 * N;
-      float2 v = make_float2(0.f, 0.f);
-      if (e < nvalid) {
-        v = __ldg(xb + e);
-        if (ab) v = csub(v, __ldg(ab + e));
-      }
-      xs[l3 * XS + pos] = v;
-    }
-  }
-  __syncthreads();
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
-  const float2* xr = xs + lr * XS + p;
   // software pipeline: coil j+1's map values are loaded while coil j is transformed
   float2 mcur[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) mcur[q] = valid ? __ldg(mb + P * q) : make_float2(0.f, 0.f);
+  // stage u = x - anchor for the CTA's rows once (reused by every coil); all loads of a
+  // thread are issued before the first use so their latencies overlap (T * Q = ROWS * N)
+  {
+    const float2* xb = x + b * x_bstride + (long long)row0 * N;
+    // never a null-based address, even for loads the compiler hoists above the anchor test
+    const float2* ab = anchor ? anchor + b * x_bstride + (long long)row0 * N : xb;
+    float2 v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const int e = tid + i * T;
+      v[i] = e < nvalid ? __ldg(xb + e) : make_float2(0.f, 0.f);
+    }
+    if (anchor) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const int e = tid + i * T;
+        if (e < nvalid) v[i] = csub(v[i], __ldg(ab + e));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      const int e = tid + i * T;
+      const int l3 = e / N, pos = e - l3 * N;
+      xs[l3 * XS + pos] = v[i];
+    }
+  }
+  __syncthreads();
+  const float2* xr = xs + lr * XS + p;
   for (int j = 0; j < ncoils; ++j) {
     float2 r[Q];
 #pragma unroll
@@ -247,12 +259,15 @@ struct ColCfg {
   static constexpr int VSP = FftShape<P, Q>::VS0 | 1;  // odd stride: conflict-free over columns
 };
 
-template <int P, int Q>
+// NXC > 0: row length known at compile time (square images) -> immediate address offsets
+template <int P, int Q, int NXC>
 __global__ void __launch_bounds__(ColCfg<P, Q>::T)
 k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long mask_bstride,
-          float mscale, int mode, int nx, int ncoils) {
+          float mscale, int mode, int nx_rt, int ncoils) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, CB = ColCfg<P, Q>::CB, T = ColCfg<P, Q>::T, VSP = ColCfg<P, Q>::VSP;
+  constexpr bool FULL = NXC > 0 && (NXC % CB) == 0;  // every column block is complete
+  const int nx = NXC > 0 ? NXC : nx_rt;
   extern __shared__ float2 smem[];
   float2* t1 = smem;
   float2* t2 = smem + N;
@@ -262,12 +277,12 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
   const int j = blockIdx.y, b = blockIdx.z;
   const long long D = (long long)nx * N;
   float2* img = ws + ((long long)b * ncoils + j) * D;
-  const int ncols = min(CB, nx - c0);
+  const int ncols = FULL ? CB : min(CB, nx - c0);
   init_tw_s1<P, Q>(t1, tid, T);
   init_tw_s2<P, Q>(t2, tid, T);
   __syncthreads();
   const int c = tid % CB, p = tid / CB;
-  const bool cvalid = c < ncols;
+  const bool cvalid = FULL || c < ncols;
 
   if (mode == COL_INV) {
     // spectrum in perm order along y -> smem
@@ -340,6 +355,84 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
   if (cvalid) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) img[(long long)(p + P * q) * nx + c0 + c] = r[q];
+  }
+}
+
+// Column pass of the normal operator, several coils per CTA: the mask words of the
+// CTA's (column, k2) groups are loaded once, and coil j+1's column strip is loaded into
+// registers while coil j is transformed (the load latency is hidden behind steps 2/3).
+// Requires CB * Q <= T (one step-2 group per thread) and full column blocks.
+template <int P, int Q, int NXC>
+__global__ void __launch_bounds__(ColCfg<P, Q>::T, 2)
+k_colnormal(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long mask_bstride,
+            int ncoils, int jc) {
+  using S = FftShape<P, Q>;
+  constexpr int N = S::N, CB = ColCfg<P, Q>::CB, T = ColCfg<P, Q>::T, VSP = ColCfg<P, Q>::VSP;
+  constexpr int NX = NXC;
+  static_assert(NX % CB == 0 && CB * Q <= T && (P % 4) == 0, "k_colnormal shape");
+  constexpr long long D = (long long)NX * N;
+  extern __shared__ float2 smem[];
+  float2* t1 = smem;
+  float2* t2 = smem + N;
+  float2* buf = smem + 2 * N;
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * CB;
+  const int j0 = blockIdx.y * jc, j1 = min(ncoils, j0 + jc);
+  const int b = blockIdx.z;
+  init_tw_s1<P, Q>(t1, tid, T);
+  init_tw_s2<P, Q>(t2, tid, T);
+  const int c = tid % CB, p = tid / CB;
+  // step-2 task of this thread: column cc, group k2
+  const int cc = tid % CB, k2 = tid / CB;
+  const bool s2 = tid < CB * Q;
+  uint32_t mw[P / 4];
+  {
+    const uint32_t* mk = reinterpret_cast<const uint32_t*>(maskT + b * mask_bstride +
+                                                           (long long)(c0 + cc) * N + P * k2);
+#pragma unroll
+    for (int w4 = 0; w4 < P / 4; ++w4) mw[w4] = s2 ? __ldg(mk + w4) : 0u;
+  }
+  float2* img0 = ws + ((long long)b * ncoils) * D + (long long)p * NX + c0 + c;
+  float2 rn[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) rn[q] = img0[j0 * D + (long long)(P * q) * NX];
+  __syncthreads();
+  for (int j = j0; j < j1; ++j) {
+    float2* img = img0 + j * D;
+    float2 r[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) r[q] = rn[q];
+    fft_s1_fwd<P, Q>(r, p, t1);
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk) buf[c * VSP + S::GS * kk + p] = r[kk];
+    if (j + 1 < j1) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) rn[q] = img[D + (long long)(P * q) * NX];
+    }
+    __syncthreads();
+    if (s2) {
+      float2 g[P];
+      float2* gp = buf + cc * VSP + S::GS * k2;
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+      fft_s2_fwd<P>(g);
+#pragma unroll
+      for (int w4 = 0; w4 < P / 4; ++w4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (!((mw[w4] >> (8 * i)) & 0xffu)) g[4 * w4 + i] = make_float2(0.f, 0.f);
+      }
+      fft_s2_inv<P, Q>(g, k2, t2);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < Q; ++kk) r[kk] = buf[c * VSP + S::GS * kk + p];
+    fft_s1_inv<Q>(r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) img[(long long)(P * q) * NX] = r[q];
+    __syncthreads();  // buf is rewritten by the next coil's step 1
   }
 }
 
@@ -434,22 +527,50 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
   return SR_OK;
 }
 
-template <int P, int Q>
-int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
-                   int batch, int ncoils, int nx, cudaStream_t st) {
+template <int P, int Q, int NXC>
+int launch_colpass_t(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
+                     int batch, int ncoils, int nx, cudaStream_t st) {
   using C = ColCfg<P, Q>;
   const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(k_colpass<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k_colpass<P, Q, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
       return SR_ECUDA;
     configured = true;
   }
   dim3 grid((nx + C::CB - 1) / C::CB, ncoils, batch);
-  k_colpass<P, Q><<<grid, C::T, smem, st>>>(ws, maskT, mbs, mscale, mode, nx, ncoils);
+  k_colpass<P, Q, NXC><<<grid, C::T, smem, st>>>(ws, maskT, mbs, mscale, mode, nx, ncoils);
   SR_CHECK_LAUNCH();
   return SR_OK;
+}
+
+int g_col_jc = 4;  // coils per CTA of k_colnormal (0 = use k_colpass)
+
+template <int P, int Q>
+int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
+                   int batch, int ncoils, int nx, cudaStream_t st) {
+  using C = ColCfg<P, Q>;
+  if constexpr (P > 1 && (P % 4) == 0 && ((P * Q) % C::CB) == 0 && C::CB * Q <= C::T) {
+    if (mode == COL_NORMAL && mscale == 1.f && nx == P * Q && g_col_jc > 0) {
+      const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
+      static bool configured = false;
+      if (!configured) {
+        if (cudaFuncSetAttribute(k_colnormal<P, Q, P * Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+          return SR_ECUDA;
+        configured = true;
+      }
+      const int jc = g_col_jc < ncoils ? g_col_jc : ncoils;
+      dim3 grid(nx / C::CB, (ncoils + jc - 1) / jc, batch);
+      k_colnormal<P, Q, P * Q><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
+      SR_CHECK_LAUNCH();
+      return SR_OK;
+    }
+  }
+  if (nx == P * Q && P > 1)
+    return launch_colpass_t<P, Q, P * Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+  return launch_colpass_t<P, Q, 0>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
 }
 
 int dispatch_rowfwd(int nx, const float2* x, const float2* anchor, const float2* maps,
@@ -505,6 +626,12 @@ bool fft_size_supported(int n) {
 extern "C" {
 
 int sr_fft_size_supported(int n) { return fft_size_supported(n) ? 1 : 0; }
+
+int sr_cart_tune(int col_jc) {
+  if (col_jc < 0) return SR_EINVAL;
+  g_col_jc = col_jc;
+  return SR_OK;
+}
 
 int sr_fft_split(int n, int* P, int* Q) {
   switch (n) {

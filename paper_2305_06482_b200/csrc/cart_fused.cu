@@ -148,13 +148,13 @@ __device__ void item_rowfwd(const FusedArgs& a, int s, int rt, int j0, int j1, f
   const int nvalid = nrows * NX;
   {
     const float2* xb = a.x + (long long)s * D + (long long)rt * TILE * NX;
-    const float2* ab = a.anchor ? a.anchor + (long long)s * D + (long long)rt * TILE * NX : nullptr;
+    const float2* ab = a.anchor ? a.anchor + (long long)s * D + (long long)rt * TILE * NX : xb;
     for (int e = tid; e < TILE * NX; e += T) {
       const int l3 = e / NX, pos = e - l3 * NX;
       float2 v = make_float2(0.f, 0.f);
       if (e < nvalid) {
         v = __ldg(xb + e);
-        if (ab) v = csub(v, __ldg(ab + e));
+        if (a.anchor) v = csub(v, __ldg(ab + e));
       }
       xs[l3 * XS + pos] = v;
     }

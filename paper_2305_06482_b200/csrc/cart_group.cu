@@ -212,11 +212,12 @@ k_cart_group(const GroupArgs a) {
     const long long xo = (long long)b * D + (long long)row * NX + p;
     const float2* mr = a.maps + b * a.map_bstride + j * D + (long long)row * NX + p;
     const uint64_t keep = pol_last();
+    const float2* abase = a.anchor ? a.anchor : a.x;  // never null-based, even if hoisted
     float2 r[QX];
 #pragma unroll
     for (int q = 0; q < QX; ++q) {
       float2 v = ld_nc_hint(a.x + xo + PX * q, keep);
-      if (a.anchor) v = csub(v, ld_nc_hint(a.anchor + xo + PX * q, keep));
+      if (a.anchor) v = csub(v, ld_nc_hint(abase + xo + PX * q, keep));
       r[q] = cmul(ld_nc_hint(mr + PX * q, keep), v);
     }
     fft_s1_fwd<PX, QX>(r, p, tx1);

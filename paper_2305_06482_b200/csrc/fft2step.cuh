@@ -21,6 +21,7 @@
 #pragma once
 #include "common.cuh"
 #include "dft_gen.cuh"
+#include "tw_gen.cuh"
 
 template <int P_, int Q_>
 struct FftShape {
@@ -37,27 +38,22 @@ struct FftShape {
   __host__ __device__ __forceinline__ static int perm_pos(int k) { return P_ * (k % Q_) + k / Q_; }
 };
 
-// Twiddle tables (fp32 sincospif of an exactly reduced argument, |err| ~ 1 ulp):
+// Twiddle tables, copied into shared memory from the generated constants of
+// tw_gen.cuh (float64 -> float32, correctly rounded):
 //   t1[k2*P + p] = W_N^{p k2}   (forward step 1; lanes vary p  -> conflict-free)
 //   t2[m1*Q + k2] = W_N^{m1 k2} (inverse step 2'; lanes vary k2 -> conflict-free)
 template <int P, int Q>
 __device__ __forceinline__ void init_tw_s1(float2* t1, int tid, int nthreads) {
-  constexpr int N = P * Q;
-  for (int e = tid; e < N; e += nthreads) {
-    const int k2 = e / P, p = e - k2 * P;
-    float s, c;
-    sincospif(-2.0f * (float)(p * k2) / (float)N, &s, &c);
-    t1[e] = make_float2(c, s);
+  if constexpr (P > 1) {
+    const float2* src = TwTab<P, Q>::t1();
+    for (int e = tid; e < P * Q; e += nthreads) t1[e] = __ldg(src + e);
   }
 }
 template <int P, int Q>
 __device__ __forceinline__ void init_tw_s2(float2* t2, int tid, int nthreads) {
-  constexpr int N = P * Q;
-  for (int e = tid; e < N; e += nthreads) {
-    const int m1 = e / Q, k2 = e - m1 * Q;
-    float s, c;
-    sincospif(-2.0f * (float)(m1 * k2) / (float)N, &s, &c);
-    t2[e] = make_float2(c, s);
+  if constexpr (P > 1) {
+    const float2* src = TwTab<P, Q>::t2();
+    for (int e = tid; e < P * Q; e += nthreads) t2[e] = __ldg(src + e);
   }
 }
 

@@ -200,11 +200,52 @@ def generate() -> str:
     return "\n".join(parts)
 
 
-def main(argv):
-    out = Path(argv[1]) if len(argv) > 1 else Path(__file__).with_name("dft_gen.cuh")
-    text = generate()
+def fft_sizes() -> list[tuple[int, int, int]]:
+    """(N, P, Q) of the SR_FFT_SIZES table in fft2step.cuh (single source of truth)."""
+    import re
+    text = Path(__file__).with_name("fft2step.cuh").read_text()
+    lines = text[text.index("#define SR_FFT_SIZES(X)"):].splitlines()
+    n = next(i for i, ln in enumerate(lines) if not ln.rstrip().endswith("\\"))
+    body = "\n".join(lines[: n + 1])
+    return [tuple(int(v) for v in m) for m in re.findall(r"X\((\d+),\s*(\d+),\s*(\d+)\)", body)]
+
+
+def generate_twiddles() -> str:
+    """Inter-stage twiddle tables of the two-level FFT, float64 -> float32 once:
+    t1[k2*P + p] = W_N^{p k2},  t2[m1*Q + k2] = W_N^{m1 k2},  W_N = exp(-2 pi i / N)."""
+    parts = [
+        "// AUTO-GENERATED by gen_dft.py -- do not edit.\n"
+        "// Two-level FFT twiddle tables (see fft2step.cuh), float64 -> float32.\n"
+        "#pragma once\n#include <cuda_runtime.h>\n",
+        "template <int P, int Q> struct TwTab;\n",
+    ]
+    for n, p, q in fft_sizes():
+        if p == 1:
+            continue
+
+        def w(k):
+            a = -2.0 * math.pi * (k % n) / n
+            return f"{{{_fmt(math.cos(a))}, {_fmt(math.sin(a))}}}"
+
+        t1 = ", ".join(w(pp * k2) for k2 in range(q) for pp in range(p))
+        t2 = ", ".join(w(m1 * k2) for m1 in range(p) for k2 in range(q))
+        parts.append(f"static __device__ const float2 sr_tw1_{n}[{n}] = {{{t1}}};\n"
+                     f"static __device__ const float2 sr_tw2_{n}[{n}] = {{{t2}}};\n"
+                     f"template <> struct TwTab<{p}, {q}> {{\n"
+                     f"  __device__ __forceinline__ static const float2* t1() {{ return sr_tw1_{n}; }}\n"
+                     f"  __device__ __forceinline__ static const float2* t2() {{ return sr_tw2_{n}; }}\n}};\n")
+    return "\n".join(parts)
+
+
+def _write(out: Path, text: str) -> None:
     if not out.exists() or out.read_text() != text:
         out.write_text(text)
+
+
+def main(argv):
+    out = Path(argv[1]) if len(argv) > 1 else Path(__file__).with_name("dft_gen.cuh")
+    _write(out, generate())
+    _write(out.with_name("tw_gen.cuh"), generate_twiddles())
 
 
 if __name__ == "__main__":

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--chunks", default="0,32,16")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--fused", default="", help="semicolon list of lagB,lagC,slots,tile configs of the persistent launch")
+    ap.add_argument("--coljc", default="", help="comma list of column-pass coils per CTA (0 = generic)")
     ap.add_argument("--group", default="", help="comma list of group sizes G for chunk -2")
     ap.add_argument("--stats", action="store_true", help="collect fused-kernel wait/item statistics")
     ap.add_argument("--multistream", default="", help="semicolon list of chunk,streams for the three-pass schedule")
@@ -51,6 +52,14 @@ def main():
         ch, ns = (int(v) for v in cfg.split(","))
         ms = multistream(kern, smaps, x, out, ch, ns)
         print(json.dumps({"multistream": cfg, "ms_per_apply": ms}), flush=True)
+    for jc in [int(c) for c in args.coljc.split(",") if c]:
+        _lib.call("sr_cart_tune", jc)
+        t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=0), args.steps, 3, torch.cuda.synchronize)
+        ms = t / args.steps * 1e3
+        print(json.dumps({"coljc": jc, "ms_per_apply": ms, "alg_GBps": bench.algorithmic_bytes() / (ms * 1e-3) / 1e9}),
+              flush=True)
+    if args.coljc:
+        _lib.call("sr_cart_tune", 4)
     for g in [int(c) for c in args.group.split(",") if c]:
         _lib.call("sr_group_select", g)
         t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=-2), args.steps, 3, torch.cuda.synchronize)
