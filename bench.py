@@ -333,16 +333,26 @@ def main():
     ms = t_s / args.steps * 1e3
     bytes_apply = algorithmic_bytes()
     peak, peak_kind = measured_peak()
-    traffic = None
+    traffic, inst = None, None
     tp = ROOT / "profiles" / "k1_traffic.json"
     if tp.exists():
         try:
-            traffic = float(json.loads(tp.read_text())["traffic_bytes"])
+            prof = json.loads(tp.read_text())
+            traffic = float(prof["traffic_bytes"])
+            inst = float(prof.get("warp_instructions")) if prof.get("warp_instructions") else None
         except Exception:
-            traffic = None
+            traffic, inst = None, None
     achieved = bytes_apply / (t_s / args.steps) / 1e9
     if rank == 0:
         cpu = None if args.no_cpu_baseline else cpu_baseline_single(args.seed)
+        clocks = clk.summary()
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        sm_hz = (clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965) * 1e6
+        # the two floors of this three-launch schedule: HBM bytes actually moved (ncu) at the
+        # measured peak, and warp instructions (ncu) at one issue per SMSP per cycle
+        floors = {"dram_ms": None if traffic is None else traffic / (peak * 1e9) * 1e3,
+                  "issue_ms": None if inst is None else inst / (nsm * 4 * sm_hz) * 1e3,
+                  "warp_instructions_per_apply": inst}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -362,11 +372,11 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per apply "
                                            "(profiles/k1_traffic.json)",
-                         "kernel": "K1 fused sketched normal op (rowfwd + colpass + rowinv launches)",
-                         "algorithmic_bytes_per_apply": bytes_apply},
+                         "kernel": "K1 fused sketched normal op (rowfwd + colnormal + rowinv launches)",
+                         "algorithmic_bytes_per_apply": bytes_apply, "floors": floors},
             "gpu_launches": 3 * args.steps,
             "e2e_gpu_launches_per_step": 3 * 8,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
