@@ -487,8 +487,21 @@ struct BinCfg {
 };
 
 // 0 normal (interp, *w, spread), 1 forward (interp -> y), 2 adjoint (spread y).
-// One warp per sample, lanes over the W^ND taps: no two lanes of a warp touch the
-// same cell, so the shared accumulator only sees contention between the 8 warps.
+// Pass 1 (interp): L lanes per sample, each owning RPL rows (a0, a1) of W taps along the
+// contiguous axis; the partial sums are reduced over the L lanes (log2 L shuffles).  With the
+// odd tile pitch TB the 8 row starts of a W = 4 sample fall in distinct banks.
+// Pass 2 (spread): warp per sample, lanes over taps, into a fixed-point int32 tile with native
+// shared atomics (exact and order independent within the tile), converted back to float at
+// the flush (one global float2 atomic per touched cell).
+template <int ND, int W>
+struct BinLanes {
+  static constexpr int W0 = (ND == 3) ? W : 1;
+  static constexpr int ROWS = W0 * W;  // (a0, a1) rows of a sample
+  static constexpr int L = (ROWS % 8 == 0) ? 8 : ((ROWS % 4 == 0) ? 4 : ((ROWS % 2 == 0) ? 2 : 1));
+  static constexpr int RPL = ROWS / L;
+  static constexpr int SPW = 32 / L;  // samples per warp
+};
+
 template <int MODE, int ND, int W, int B>
 __global__ void __launch_bounds__(BIN_THREADS)
 k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int* __restrict__ base,
@@ -496,41 +509,62 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
              long long N, const int* __restrict__ chunks, NufftGeom g, int ncoils, float scale,
              float2* __restrict__ y, const float2* __restrict__ ymeas, double* __restrict__ partial) {
   using C = BinCfg<ND, W, B>;
-  constexpr int CELLS = C::CELLS, T1 = C::T1, T2 = C::T2, NTAPS = C::NTAPS;
+  using LN = BinLanes<ND, W>;
+  constexpr int CELLS = C::CELLS, T1 = C::T1, T2 = C::T2;
   constexpr int A0 = 3 - ND;  // first active axis
+  constexpr int L = LN::L, RPL = LN::RPL, SPW = LN::SPW;
+  constexpr int NWARPS = BIN_THREADS / 32;
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* tile = reinterpret_cast<float2*>(smraw);                       // spectrum tile (modes 0, 1)
-  float2* acc = tile + ((MODE == 2) ? 0 : CELLS);                         // spread accumulator (0, 2)
-  float* wts = reinterpret_cast<float*>(acc + ((MODE == 1) ? 0 : CELLS));  // [3][W][BIN_CHUNK]
-  short* loc = reinterpret_cast<short*>(wts + 3 * W * BIN_CHUNK);          // [3][BIN_CHUNK]
-  int* coff = reinterpret_cast<int*>(loc + 3 * BIN_CHUNK + 2);             // [CELLS] grid offsets
+  float2* tile = reinterpret_cast<float2*>(smraw);                         // spectrum tile (modes 0, 1)
+  int2* acc = reinterpret_cast<int2*>(tile + ((MODE == 2) ? 0 : CELLS));    // fixed-point spread (0, 2)
+  float2* sv = reinterpret_cast<float2*>(acc + ((MODE == 1) ? 0 : CELLS));  // [BIN_CHUNK] sample values
+  constexpr int WS = 3 * W + 1;                                             // odd per-sample stride
+  float* wts = reinterpret_cast<float*>(sv + BIN_CHUNK);                   // [BIN_CHUNK][WS]
+  float* swi = wts + WS * BIN_CHUNK;                                       // [BIN_CHUNK] sqrt weights
+  float* swm = swi + BIN_CHUNK;                                            // [BIN_CHUNK] max tap weight
+  int* soi = reinterpret_cast<int*>(swm + BIN_CHUNK);                      // [BIN_CHUNK] output index
+  int* scb = soi + BIN_CHUNK;                                              // [BIN_CHUNK] first-tap cell
+  int* coff = scb + BIN_CHUNK;                                             // [CELLS] grid offsets
+  __shared__ float s_red[NWARPS];
   const int* ch = chunks + 5 * blockIdx.x;
   const int org0 = ch[0], org1 = ch[1], org2 = ch[2];
   const int s0 = ch[3], ns = ch[4];
   const int tid = threadIdx.x;
   const long long sg12 = (long long)g.g[1] * g.g[2];
-  // per-sample KB weights and local tap origins (once, reused by every coil)
+  // per-sample KB weights, local tap origins, density weight, output index and the largest
+  // tap weight (once per chunk, reused by every coil)
   for (int i = tid; i < ns; i += BIN_THREADS) {
     const long long sidx = s0 + i;
+    swi[i] = wgt ? wgt[sidx] : 1.f;
+    soi[i] = orig ? orig[sidx] : (int)sidx;
+    float wm = 1.f;
+    int lc[3] = {0, 0, 0};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       if (a < A0) {
-        loc[a * BIN_CHUNK + i] = 0;
 #pragma unroll
-        for (int k = 0; k < W; ++k) wts[(a * W + k) * BIN_CHUNK + i] = (k == 0) ? 1.f : 0.f;
+        for (int k = 0; k < W; ++k) wts[i * WS + a * W + k] = (k == 0) ? 1.f : 0.f;
         continue;
       }
       int bb = base[a * N + sidx] % g.g[a];
       if (bb < 0) bb += g.g[a];
       int l = bb - (a == 0 ? org0 : (a == 1 ? org1 : org2));
       if (l < 0) l += g.g[a];
-      loc[a * BIN_CHUNK + i] = (short)l;
+      lc[a] = l;
       const float t = frac[a * N + sidx];
+      float m = 0.f;
 #pragma unroll
-      for (int k = 0; k < W; ++k) wts[(a * W + k) * BIN_CHUNK + i] = kb_weight(t - (float)k, g.beta[a], (float)W);
+      for (int k = 0; k < W; ++k) {
+        const float wk = kb_weight(t - (float)k, g.beta[a], (float)W);
+        wts[i * WS + a * W + k] = wk;
+        m = fmaxf(m, wk);
+      }
+      wm *= m;
     }
+    swm[i] = wm;
+    scb[i] = (lc[0] * T1 + lc[1]) * T2 + lc[2];
   }
-  auto cell_off = [&](int e) -> long long {
+  for (int e = tid; e < CELLS; e += BIN_THREADS) {
     const int c2 = e % T2, c1 = (e / T2) % T1, c0 = e / (T2 * T1);
     int k0 = org0 + c0, k1 = org1 + c1, k2 = org2 + c2;
     k0 -= (k0 >= g.g[0]) ? g.g[0] : 0;
@@ -539,82 +573,106 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
     if (k0 >= g.g[0]) k0 %= g.g[0];  // tiles wider than the grid (tiny grids)
     if (k1 >= g.g[1]) k1 %= g.g[1];
     if (k2 >= g.g[2]) k2 %= g.g[2];
-    return (long long)perm_of(k0, g.P[0], g.Q[0]) * sg12 + (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] +
-           perm_of(k2, g.P[2], g.Q[2]);
-  };
-  for (int e = tid; e < CELLS; e += BIN_THREADS) coff[e] = (int)cell_off(e);  // once per chunk
+    coff[e] = (int)((long long)perm_of(k0, g.P[0], g.Q[0]) * sg12 +
+                    (long long)perm_of(k1, g.P[1], g.Q[1]) * g.g[2] + perm_of(k2, g.P[2], g.Q[2]));
+  }
   const int lane = tid & 31, warp = tid >> 5;
-  constexpr int NWARPS = BIN_THREADS / 32;
+  const int sub = lane % L, slot = lane / L;
   double acc2 = 0.0;
   for (int j = 0; j < ncoils; ++j) {
     const long long go = (long long)j * g.G;
     __syncthreads();
     for (int e = tid; e < CELLS; e += BIN_THREADS) {
       if (MODE != 2) tile[e] = src[go + coff[e]];
-      if (MODE != 1) acc[e] = make_float2(0.f, 0.f);
+      if (MODE != 1) acc[e] = make_int2(0, 0);
     }
     __syncthreads();
-    for (int i = warp; i < ns; i += NWARPS) {
-      const int l0 = loc[i], l1 = loc[BIN_CHUNK + i], l2 = loc[2 * BIN_CHUNK + i];
-      const int cbase = (l0 * T1 + l1) * T2 + l2;
-      const long long sidx = s0 + i;
-      float2 v = make_float2(0.f, 0.f);
-      if (MODE != 2) {
+    // pass 1: the value of every sample (interp: L lanes per sample)
+    if (MODE != 2) {
+      for (int i0 = warp * SPW; i0 < ns; i0 += NWARPS * SPW) {
+        const int i = i0 + slot;
+        const bool has = i < ns;
+        const int ii = has ? i : i0;
+        const int cbase = scb[ii];
+        const float* wi_ = wts + ii * WS;
+        float2 v = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int t0 = 0; t0 < NTAPS; t0 += 32) {
-          const int t = t0 + lane;
-          if (NTAPS % 32 == 0 || t < NTAPS) {
-            const int a2 = t % W, a1 = (t / W) % W, a0 = (ND == 3) ? t / (W * W) : 0;
-            const float wt = wts[(a0) * BIN_CHUNK + i] * wts[(W + a1) * BIN_CHUNK + i] *
-                             wts[(2 * W + a2) * BIN_CHUNK + i];
-            const float2 sv = tile[cbase + (a0 * T1 + a1) * T2 + a2];
-            v.x = fmaf(wt, sv.x, v.x);
-            v.y = fmaf(wt, sv.y, v.y);
+        for (int k = 0; k < RPL; ++k) {
+          const int r = sub * RPL + k, a0 = r / W, a1 = r - a0 * W;
+          const float wr = wi_[a0] * wi_[W + a1];
+          const float2* row = tile + cbase + (a0 * T1 + a1) * T2;
+#pragma unroll
+          for (int a2 = 0; a2 < W; ++a2) {
+            const float wt = wr * wi_[2 * W + a2];
+            const float2 tv = row[a2];
+            v.x = fmaf(wt, tv.x, v.x);
+            v.y = fmaf(wt, tv.y, v.y);
           }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = L / 2; o > 0; o >>= 1) {
           v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
           v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
         }
-      }
-      const float wi = wgt ? wgt[sidx] : 1.f;
-      if (MODE == 1) {
-        if (lane == 0) {
-          const long long oi = orig ? orig[sidx] : sidx;
-          float2 yv = cscale(v, wi * scale);
+        if (!has || sub != 0) continue;
+        const float2 vs = cscale(v, swi[i] * scale);
+        if (MODE == 1) {
+          const long long oi = soi[i];
+          float2 yv = vs;
           if (ymeas) {
             yv = csub(yv, ymeas[(long long)j * N + oi]);
             acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
           }
           y[(long long)j * N + oi] = yv;
+        } else {
+          sv[i] = vs;
         }
-        continue;
       }
-      if (MODE == 0) {
-        v = cscale(v, wi * scale);
-      } else {
-        const long long oi = orig ? orig[sidx] : sidx;
-        v = cscale(y[(long long)j * N + oi], wi * scale);
-      }
+    } else {
+      for (int i = tid; i < ns; i += BIN_THREADS) sv[i] = cscale(y[(long long)j * N + soi[i]], swi[i] * scale);
+    }
+    if (MODE == 1) continue;
+    // fixed-point scale: every cell sum is bounded by B = sum_s max(|re|, |im|) * max tap weight;
+    // integers are scaled so that B maps below 2^30 (int32 shared atomics are native, exact and
+    // order independent; a float CAS loop retries under contention)
+    __syncthreads();
+    float bsum = 0.f;
+    for (int i = tid; i < ns; i += BIN_THREADS) bsum += fmaxf(fabsf(sv[i].x), fabsf(sv[i].y)) * swm[i];
 #pragma unroll
-      for (int t0 = 0; t0 < NTAPS; t0 += 32) {
+    for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    if (lane == 0) s_red[warp] = bsum;
+    __syncthreads();
+    float bnd = 0.f;
+#pragma unroll
+    for (int w = 0; w < NWARPS; ++w) bnd += s_red[w];
+    bnd *= 1.0001f;  // float rounding of the bound itself
+    if (!(bnd > 0.f)) continue;  // nothing to spread (all zero)
+    int ex;
+    frexpf(bnd, &ex);  // bnd < 2^ex
+    const int S = min(126, max(-126, 30 - ex));
+    const float up = ldexpf(1.f, S), down = ldexpf(1.f, -S);
+    // pass 2: spread, one sample at a time per warp, lanes over taps (distinct cells)
+    for (int i = warp; i < ns; i += NWARPS) {
+      const float2 v = cscale(sv[i], up);
+      const int cb = scb[i];
+      const float* wi_ = wts + i * WS;
+#pragma unroll
+      for (int t0 = 0; t0 < C::NTAPS; t0 += 32) {
         const int t = t0 + lane;
-        if (NTAPS % 32 == 0 || t < NTAPS) {
+        if (C::NTAPS % 32 == 0 || t < C::NTAPS) {
           const int a2 = t % W, a1 = (t / W) % W, a0 = (ND == 3) ? t / (W * W) : 0;
-          const float wt = wts[(a0) * BIN_CHUNK + i] * wts[(W + a1) * BIN_CHUNK + i] *
-                           wts[(2 * W + a2) * BIN_CHUNK + i];
-          smem_add_f2(&acc[cbase + (a0 * T1 + a1) * T2 + a2], cscale(v, wt));
+          const float wt = wi_[a0] * wi_[W + a1] * wi_[2 * W + a2];
+          int2* cell = &acc[cb + (a0 * T1 + a1) * T2 + a2];
+          atomicAdd(&cell->x, __float2int_rn(v.x * wt));
+          atomicAdd(&cell->y, __float2int_rn(v.y * wt));
         }
       }
     }
-    if (MODE != 1) {
-      __syncthreads();
-      for (int e = tid; e < CELLS; e += BIN_THREADS) {
-        const float2 av = acc[e];
-        if (av.x == 0.f && av.y == 0.f) continue;
-        red_add_f2(dst + go + coff[e], av);
-      }
+    __syncthreads();
+    for (int e = tid; e < CELLS; e += BIN_THREADS) {
+      const int2 av = acc[e];
+      if (av.x == 0 && av.y == 0) continue;
+      red_add_f2(dst + go + coff[e], make_float2((float)av.x * down, (float)av.y * down));
     }
   }
   if (MODE == 1 && partial) {
@@ -634,8 +692,9 @@ int launch_bins_t(const float2* src, float2* dst, const int* base, const float* 
                   const int* orig, long long N, const int* chunks, int nchunks, const NufftGeom& g, int ncoils,
                   float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
   using C = BinCfg<ND, W, B>;
-  const size_t smem = sizeof(float2) * C::CELLS * ((MODE == 0) ? 2 : 1) + sizeof(float) * 3 * W * BIN_CHUNK +
-                      sizeof(short) * (3 * BIN_CHUNK + 2) + sizeof(int) * C::CELLS + 16;
+  const size_t smem = sizeof(float2) * C::CELLS * ((MODE == 0) ? 2 : 1) + sizeof(float2) * BIN_CHUNK +
+                      sizeof(float) * (3 * W + 1 + 2) * BIN_CHUNK + sizeof(int) * 2 * BIN_CHUNK +
+                      sizeof(int) * C::CELLS + 16;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(k_nufft_bins<MODE, ND, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -717,6 +776,7 @@ unsigned sample_blocks(long long N) {
 }  // namespace
 
 extern "C" {
+
 
 // Plan arrays (device): base (3, N) int32 tap bases (fp64-derived, ceil(u - w/2)),
 // frac (3, N) fp32 offsets u - base, wgt (N) = density weight w (normal op) and
