@@ -502,6 +502,19 @@ struct BinLanes {
   static constexpr int SPW = 32 / L;  // samples per warp
 };
 
+constexpr int BIN_CPB = 1;  // coils per pass (2 shares tap weights over a pair but drops to 3 CTAs/SM: no gain measured)
+
+template <int MODE, int ND, int W, int B>
+struct BinSmem {
+  using C = BinCfg<ND, W, B>;
+  static constexpr int WS = 3 * W + 1;  // odd per-sample stride of the tap weights
+  static constexpr size_t TILE = (MODE == 2) ? 0 : sizeof(float2) * BIN_CPB * C::CELLS;
+  static constexpr size_t ACC = (MODE == 1) ? 0 : sizeof(int2) * BIN_CPB * C::CELLS;
+  static constexpr size_t SV = sizeof(float2) * BIN_CPB * BIN_CHUNK;
+  static constexpr size_t PER = sizeof(float) * (WS + 2) * BIN_CHUNK + sizeof(int) * 2 * BIN_CHUNK;
+  static constexpr size_t BYTES = TILE + ACC + SV + PER + sizeof(int) * C::CELLS + 16;
+};
+
 template <int MODE, int ND, int W, int B>
 __global__ void __launch_bounds__(BIN_THREADS)
 k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int* __restrict__ base,
@@ -510,29 +523,30 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
              float2* __restrict__ y, const float2* __restrict__ ymeas, double* __restrict__ partial) {
   using C = BinCfg<ND, W, B>;
   using LN = BinLanes<ND, W>;
+  using SM = BinSmem<MODE, ND, W, B>;
   constexpr int CELLS = C::CELLS, T1 = C::T1, T2 = C::T2;
   constexpr int A0 = 3 - ND;  // first active axis
   constexpr int L = LN::L, RPL = LN::RPL, SPW = LN::SPW;
   constexpr int NWARPS = BIN_THREADS / 32;
+  constexpr int CPB = BIN_CPB, WS = SM::WS;
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* tile = reinterpret_cast<float2*>(smraw);                         // spectrum tile (modes 0, 1)
-  int2* acc = reinterpret_cast<int2*>(tile + ((MODE == 2) ? 0 : CELLS));    // fixed-point spread (0, 2)
-  float2* sv = reinterpret_cast<float2*>(acc + ((MODE == 1) ? 0 : CELLS));  // [BIN_CHUNK] sample values
-  constexpr int WS = 3 * W + 1;                                             // odd per-sample stride
-  float* wts = reinterpret_cast<float*>(sv + BIN_CHUNK);                   // [BIN_CHUNK][WS]
-  float* swi = wts + WS * BIN_CHUNK;                                       // [BIN_CHUNK] sqrt weights
-  float* swm = swi + BIN_CHUNK;                                            // [BIN_CHUNK] max tap weight
-  int* soi = reinterpret_cast<int*>(swm + BIN_CHUNK);                      // [BIN_CHUNK] output index
-  int* scb = soi + BIN_CHUNK;                                              // [BIN_CHUNK] first-tap cell
-  int* coff = scb + BIN_CHUNK;                                             // [CELLS] grid offsets
+  float2* tile = reinterpret_cast<float2*>(smraw);                  // [CPB][CELLS] spectrum (modes 0, 1)
+  int2* acc = reinterpret_cast<int2*>(smraw + SM::TILE);            // [CPB][CELLS] fixed-point spread (0, 2)
+  float2* sv = reinterpret_cast<float2*>(smraw + SM::TILE + SM::ACC);  // [CPB][BIN_CHUNK] sample values
+  float* wts = reinterpret_cast<float*>(sv + CPB * BIN_CHUNK);     // [BIN_CHUNK][WS]
+  float* swi = wts + WS * BIN_CHUNK;                                // [BIN_CHUNK] sqrt weights
+  float* swm = swi + BIN_CHUNK;                                     // [BIN_CHUNK] max tap weight
+  int* soi = reinterpret_cast<int*>(swm + BIN_CHUNK);               // [BIN_CHUNK] output index
+  int* scb = soi + BIN_CHUNK;                                       // [BIN_CHUNK] first-tap cell
+  int* coff = scb + BIN_CHUNK;                                      // [CELLS] grid offsets
   __shared__ float s_red[NWARPS];
   const int* ch = chunks + 5 * blockIdx.x;
   const int org0 = ch[0], org1 = ch[1], org2 = ch[2];
   const int s0 = ch[3], ns = ch[4];
   const int tid = threadIdx.x;
   const long long sg12 = (long long)g.g[1] * g.g[2];
-  // per-sample KB weights, local tap origins, density weight, output index and the largest
-  // tap weight (once per chunk, reused by every coil)
+  // per-sample KB weights, first-tap cell, density weight, output index and the largest tap
+  // weight (once per chunk, reused by every coil)
   for (int i = tid; i < ns; i += BIN_THREADS) {
     const long long sidx = s0 + i;
     swi[i] = wgt ? wgt[sidx] : 1.f;
@@ -579,15 +593,28 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
   const int lane = tid & 31, warp = tid >> 5;
   const int sub = lane % L, slot = lane / L;
   double acc2 = 0.0;
-  for (int j = 0; j < ncoils; ++j) {
-    const long long go = (long long)j * g.G;
-    __syncthreads();
-    for (int e = tid; e < CELLS; e += BIN_THREADS) {
-      if (MODE != 2) tile[e] = src[go + coff[e]];
-      if (MODE != 1) acc[e] = make_int2(0, 0);
+  // the spectrum tiles of the next coil pair are gathered with cp.async while the current pair
+  // spreads (pass 2 does not read the tiles)
+  auto fetch_tiles = [&](int j0) {
+    __syncthreads();  // coff complete / previous tile readers done
+#pragma unroll
+    for (int c = 0; c < CPB; ++c) {
+      if (j0 + c >= ncoils) break;
+      const float2* sj = src + (long long)(j0 + c) * g.G;
+      for (int e = tid; e < CELLS; e += BIN_THREADS) cp_async8(tile + c * CELLS + e, sj + coff[e]);
     }
+    cp_async_commit();
+  };
+  if (MODE != 2) fetch_tiles(0);
+  for (int j0 = 0; j0 < ncoils; j0 += CPB) {
+    const int nc = min(CPB, ncoils - j0);
+    if (MODE != 1) {
+      __syncthreads();  // previous flush done
+      for (int e = tid; e < CPB * CELLS; e += BIN_THREADS) acc[e] = make_int2(0, 0);
+    }
+    if (MODE != 2) cp_async_wait<0>();
     __syncthreads();
-    // pass 1: the value of every sample (interp: L lanes per sample)
+    // pass 1: the value of every sample for each coil of the pair (interp: L lanes per sample)
     if (MODE != 2) {
       for (int i0 = warp * SPW; i0 < ns; i0 += NWARPS * SPW) {
         const int i = i0 + slot;
@@ -595,49 +622,73 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
         const int ii = has ? i : i0;
         const int cbase = scb[ii];
         const float* wi_ = wts + ii * WS;
-        float2 v = make_float2(0.f, 0.f);
+        float2 v[CPB];
+#pragma unroll
+        for (int c = 0; c < CPB; ++c) v[c] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < RPL; ++k) {
           const int r = sub * RPL + k, a0 = r / W, a1 = r - a0 * W;
           const float wr = wi_[a0] * wi_[W + a1];
-          const float2* row = tile + cbase + (a0 * T1 + a1) * T2;
+          const int ro = cbase + (a0 * T1 + a1) * T2;
 #pragma unroll
           for (int a2 = 0; a2 < W; ++a2) {
             const float wt = wr * wi_[2 * W + a2];
-            const float2 tv = row[a2];
-            v.x = fmaf(wt, tv.x, v.x);
-            v.y = fmaf(wt, tv.y, v.y);
+#pragma unroll
+            for (int c = 0; c < CPB; ++c) {
+              const float2 tv = tile[c * CELLS + ro + a2];
+              v[c].x = fmaf(wt, tv.x, v[c].x);
+              v[c].y = fmaf(wt, tv.y, v[c].y);
+            }
           }
         }
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) {
-          v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
-          v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+#pragma unroll
+          for (int c = 0; c < CPB; ++c) {
+            v[c].x += __shfl_xor_sync(0xffffffffu, v[c].x, o);
+            v[c].y += __shfl_xor_sync(0xffffffffu, v[c].y, o);
+          }
         }
         if (!has || sub != 0) continue;
-        const float2 vs = cscale(v, swi[i] * scale);
-        if (MODE == 1) {
-          const long long oi = soi[i];
-          float2 yv = vs;
-          if (ymeas) {
-            yv = csub(yv, ymeas[(long long)j * N + oi]);
-            acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
+        const float sc = swi[i] * scale;
+#pragma unroll
+        for (int c = 0; c < CPB; ++c) {
+          if (c >= nc) break;
+          const float2 vs = cscale(v[c], sc);
+          if (MODE == 1) {
+            const long long yo = (long long)(j0 + c) * N + soi[i];
+            float2 yv = vs;
+            if (ymeas) {
+              yv = csub(yv, ymeas[yo]);
+              acc2 += (double)yv.x * yv.x + (double)yv.y * yv.y;
+            }
+            y[yo] = yv;
+          } else {
+            sv[c * BIN_CHUNK + i] = vs;
           }
-          y[(long long)j * N + oi] = yv;
-        } else {
-          sv[i] = vs;
         }
       }
     } else {
-      for (int i = tid; i < ns; i += BIN_THREADS) sv[i] = cscale(y[(long long)j * N + soi[i]], swi[i] * scale);
+      for (int i = tid; i < ns; i += BIN_THREADS) {
+        const float sc = swi[i] * scale;
+#pragma unroll
+        for (int c = 0; c < CPB; ++c)
+          sv[c * BIN_CHUNK + i] = (c < nc) ? cscale(y[(long long)(j0 + c) * N + soi[i]], sc) : make_float2(0.f, 0.f);
+      }
     }
+    if (MODE != 2 && j0 + CPB < ncoils) fetch_tiles(j0 + CPB);  // (its barrier also publishes sv)
     if (MODE == 1) continue;
-    // fixed-point scale: every cell sum is bounded by B = sum_s max(|re|, |im|) * max tap weight;
-    // integers are scaled so that B maps below 2^30 (int32 shared atomics are native, exact and
-    // order independent; a float CAS loop retries under contention)
+    // fixed-point scale: every cell sum is bounded by B = sum_s max(|re|, |im|) * max tap weight
+    // (over the pair); integers are scaled so that B maps below 2^30.  int32 shared atomics are
+    // native, exact and order independent (a float CAS loop retries under contention).
     __syncthreads();
     float bsum = 0.f;
-    for (int i = tid; i < ns; i += BIN_THREADS) bsum += fmaxf(fabsf(sv[i].x), fabsf(sv[i].y)) * swm[i];
+    for (int i = tid; i < ns; i += BIN_THREADS) {
+      float m = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) m = fmaxf(m, fmaxf(fabsf(sv[c * BIN_CHUNK + i].x), fabsf(sv[c * BIN_CHUNK + i].y)));
+      bsum += m * swm[i];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
     if (lane == 0) s_red[warp] = bsum;
@@ -653,7 +704,9 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
     const float up = ldexpf(1.f, S), down = ldexpf(1.f, -S);
     // pass 2: spread, one sample at a time per warp, lanes over taps (distinct cells)
     for (int i = warp; i < ns; i += NWARPS) {
-      const float2 v = cscale(sv[i], up);
+      float2 v[CPB];
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) v[c] = cscale(sv[c * BIN_CHUNK + i], up);
       const int cb = scb[i];
       const float* wi_ = wts + i * WS;
 #pragma unroll
@@ -662,17 +715,25 @@ k_nufft_bins(const float2* __restrict__ src, float2* __restrict__ dst, const int
         if (C::NTAPS % 32 == 0 || t < C::NTAPS) {
           const int a2 = t % W, a1 = (t / W) % W, a0 = (ND == 3) ? t / (W * W) : 0;
           const float wt = wi_[a0] * wi_[W + a1] * wi_[2 * W + a2];
-          int2* cell = &acc[cb + (a0 * T1 + a1) * T2 + a2];
-          atomicAdd(&cell->x, __float2int_rn(v.x * wt));
-          atomicAdd(&cell->y, __float2int_rn(v.y * wt));
+          const int cell = cb + (a0 * T1 + a1) * T2 + a2;
+#pragma unroll
+          for (int c = 0; c < CPB; ++c) {
+            atomicAdd(&acc[c * CELLS + cell].x, __float2int_rn(v[c].x * wt));
+            atomicAdd(&acc[c * CELLS + cell].y, __float2int_rn(v[c].y * wt));
+          }
         }
       }
     }
     __syncthreads();
     for (int e = tid; e < CELLS; e += BIN_THREADS) {
-      const int2 av = acc[e];
-      if (av.x == 0 && av.y == 0) continue;
-      red_add_f2(dst + go + coff[e], make_float2((float)av.x * down, (float)av.y * down));
+      const int off = coff[e];
+#pragma unroll
+      for (int c = 0; c < CPB; ++c) {
+        if (c >= nc) break;
+        const int2 av = acc[c * CELLS + e];
+        if (av.x == 0 && av.y == 0) continue;
+        red_add_f2(dst + (long long)(j0 + c) * g.G + off, make_float2((float)av.x * down, (float)av.y * down));
+      }
     }
   }
   if (MODE == 1 && partial) {
@@ -691,10 +752,7 @@ template <int MODE, int ND, int W, int B>
 int launch_bins_t(const float2* src, float2* dst, const int* base, const float* frac, const float* wgt,
                   const int* orig, long long N, const int* chunks, int nchunks, const NufftGeom& g, int ncoils,
                   float scale, float2* y, const float2* ymeas, double* partial, cudaStream_t st) {
-  using C = BinCfg<ND, W, B>;
-  const size_t smem = sizeof(float2) * C::CELLS * ((MODE == 0) ? 2 : 1) + sizeof(float2) * BIN_CHUNK +
-                      sizeof(float) * (3 * W + 1 + 2) * BIN_CHUNK + sizeof(int) * 2 * BIN_CHUNK +
-                      sizeof(int) * C::CELLS + 16;
+  const size_t smem = BinSmem<MODE, ND, W, B>::BYTES;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(k_nufft_bins<MODE, ND, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
