@@ -138,11 +138,17 @@ def _reg_kind(reg: Regularizer) -> str:
 def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketchConfig,
                          weights: DensityWeights | None = None, solver_cfg: SolverConfig | None = None,
                          x_ref: Image | None = None, x0: Image | None = None, method: str = "auto",
-                         kernel=None) -> ReconReport:
+                         kernel=None, compress: str = "device") -> ReconReport:
     """Full coil-sketched reconstruction on the device (coil_sketch.py:220-306).
 
     ``kernel`` optionally injects the Fourier kernel (e.g. a GriddedKernel with
     BASELINE's oversampling/width), where the reference builds its own.
+    ``compress``: "device" (default) takes the PCA basis from a device Householder QR of
+    Y^H plus a C x C host SVD; "lapack" runs numpy's SVD of Y on the host as the reference
+    does.  Both give the same singular subspaces, but LAPACK fixes each singular vector's
+    phase by rounding-level details of its own bidiagonalisation, so on some inputs a few
+    PCA coils come out with a different (equally valid) phase, which changes the Rademacher
+    combinations and moves the iterates by ~1e-4 NRMSE.
     """
     if cfg.c_hat0 > data.n_coils:
         raise ValueError(f"c_hat0 = {cfg.c_hat0} exceeds the {data.n_coils} available coils")
@@ -151,12 +157,19 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     if not cfg.reuse_step_size:
         raise NotImplementedError("reuse_step_size=False is not implemented on the device path")
     kind = _reg_kind(cfg.reg)
-    maps0_dev, data0_dev, _, energy = coil_compress_device(data, maps, cfg.c_hat0)
-    a = SenseOperator(maps0_dev, data.traj, weights, method=method, kernel=kernel, shape=maps.shape)
-    y = data0_dev
-    if weights is not None and not data.weights_applied:
-        y = y * a.sqrt_w_dev.to(torch.complex64)
-    y = y.view(1, cfg.c_hat0, a.n_points)
+    if compress not in ("device", "lapack"):
+        raise ValueError(f"compress must be 'device' or 'lapack', got {compress!r}")
+    if compress == "device":
+        maps0_dev, data0_dev, _, energy = coil_compress_device(data, maps, cfg.c_hat0)
+        a = SenseOperator(maps0_dev, data.traj, weights, method=method, kernel=kernel, shape=maps.shape)
+        y = data0_dev
+        if weights is not None and not data.weights_applied:
+            y = y * a.sqrt_w_dev.to(torch.complex64)
+        y = y.view(1, cfg.c_hat0, a.n_points)
+    else:
+        data0, maps0, _, energy = coil_compress_svd(data, maps, cfg.c_hat0)
+        a = SenseOperator(maps0, data0.traj, weights, method=method, kernel=kernel)
+        y = dv.c64(a.measurement_vector(data0)).view(1, cfg.c_hat0, a.n_points)
     solver_cfg = solver_cfg or SolverConfig(tol=0.0)
     if solver_cfg.tol != 0.0:
         raise NotImplementedError("the device engine runs the fixed-count inner loop (tol = 0)")

@@ -98,17 +98,18 @@ def run_2d(cfgid: int, with_oracle: bool):
     # warm-up (plans, workspaces, first-launch costs), then the timed reconstruction
     cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps),
                             cs.CoilSketchConfig(C, cfg.sketch, reg, 1, 1), weights=weights, kernel=kern)
+    compress = "lapack" if os.environ.get("SR_HOST_COMPRESS") else "device"
     runs = []
     for _ in range(3):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         rep = cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps), cfg,
-                                      weights=weights, kernel=kern)
+                                      weights=weights, kernel=kern, compress=compress)
         torch.cuda.synchronize()
         runs.append(time.perf_counter() - t0)
     t_gpu = float(np.median(runs))
     line = {"config": cfgid, "what": f"coil-sketched recon {dims} C={C} -> {v}+{s}, {T}x{K} FISTA, {wdesc}",
-            "gpu_wall_s": t_gpu, "gpu_wall_s_runs": runs, "counts": rep.counts.get("coil_transform"),
+            "gpu_wall_s": t_gpu, "gpu_wall_s_runs": runs, "compress": compress, "counts": rep.counts.get("coil_transform"),
             "expected_counts": cs.expected_coil_transforms(cfg, so.SolverConfig(tol=0.0)),
             "objectives": [r.objective for r in rep.per_outer], "data": "synthetic"}
     if with_oracle:
