@@ -117,9 +117,10 @@ class CartesianKernel:
                   dv.ptr(self.maskT) + b0 * self.mask_bstride, self.mask_bstride, dv.ptr(out) + xo,
                   dv.ptr(ws), b1 - b0, ncoils, self.ny, self.nx, None, None, None, 0, stream)
 
-    def normal_host(self, maps, x_host, out_host, *, chunks: int = 8, buffers=None):
+    def normal_host(self, maps, x_host, out_host, *, chunks: int = 8, buffers=None, lanes: int = 1):
         """A^H A on HOST (pinned) buffers, pipelined: slice chunks are copied in, applied and
-        copied out on three streams so PCIe transfers overlap the K1 launches.
+        copied out so PCIe transfers overlap the K1 launches.  Chunk i runs its K1 on compute
+        lane i % lanes (own stream and workspace), so two small-grid K1 launches share the GPU.
 
         x_host/out_host: pinned (B, D) complex64 CPU tensors.  Returns out_host (synchronised).
         `buffers` = (x_dev, out_dev) device staging tensors to reuse across calls.
@@ -130,18 +131,25 @@ class CartesianKernel:
         ncoils, _ = self._maps_stride(maps)
         B = self.batch
         chunks = max(1, min(int(chunks), B))
+        lanes = max(1, min(int(lanes), chunks))
         bounds = [(B * i // chunks, B * (i + 1) // chunks) for i in range(chunks)]
         if buffers is None:
             buffers = (torch.empty(B, self.D, dtype=torch.complex64, device=self.device),
                        torch.empty(B, self.D, dtype=torch.complex64, device=self.device))
         xd, od = buffers
-        ws = self.workspace(ncoils, batch=max(b1 - b0 for b0, b1 in bounds), chunk=0)
+        nb = max(b1 - b0 for b0, b1 in bounds)
+        need = 8 * nb * ncoils * self.D
+        if getattr(self, "_host_ws", None) is None or len(self._host_ws) < lanes or \
+                self._host_ws[0].numel() * 8 < need:
+            self._host_ws = [torch.empty((need + 7) // 8, dtype=torch.complex64, device=self.device)
+                             for _ in range(lanes)]
         cur = torch.cuda.current_stream()
-        if not hasattr(self, "_streams"):
-            self._streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
-        s_in, s_out = self._streams
-        s_in.wait_stream(cur)
-        s_out.wait_stream(cur)
+        if getattr(self, "_host_streams", None) is None or len(self._host_streams[2]) < lanes:
+            self._host_streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device),
+                                  [torch.cuda.Stream(self.device) for _ in range(lanes)])
+        s_in, s_out, s_k = self._host_streams
+        for st in (s_in, s_out, *s_k[:lanes]):
+            st.wait_stream(cur)
         done_in = []
         for b0, b1 in bounds:
             with torch.cuda.stream(s_in):
@@ -149,15 +157,18 @@ class CartesianKernel:
                 e = torch.cuda.Event()
                 e.record(s_in)
                 done_in.append(e)
-        for (b0, b1), e in zip(bounds, done_in):
-            cur.wait_event(e)
-            self._normal_range(maps, xd, od, b0, b1, ws, cur.cuda_stream)
+        for i, ((b0, b1), e) in enumerate(zip(bounds, done_in)):
+            sk = s_k[i % lanes]
+            sk.wait_event(e)
+            self._normal_range(maps, xd, od, b0, b1, self._host_ws[i % lanes], sk.cuda_stream)
             ec = torch.cuda.Event()
-            ec.record(cur)
+            ec.record(sk)
             s_out.wait_event(ec)
             with torch.cuda.stream(s_out):
                 out_host[b0:b1].copy_(od[b0:b1], non_blocking=True)
         cur.wait_stream(s_out)
+        for st in s_k[:lanes]:
+            cur.wait_stream(st)
         return out_host
 
     def partial_shape(self, ncoils: int) -> tuple:
