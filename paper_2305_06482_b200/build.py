@@ -28,7 +28,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ftz=false", 
 
 
 def _sources():
-    return sorted(list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cpp")))
+    # largest translation units first so the parallel build's critical path is short
+    srcs = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cpp"))
+    return sorted(srcs, key=lambda p: (-p.stat().st_size * (3 if "_inst_" in p.name else 1), p.name))
 
 
 def _needs_build() -> bool:

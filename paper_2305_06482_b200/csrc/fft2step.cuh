@@ -130,9 +130,14 @@ __device__ __forceinline__ void sts_group(float2* gp, const float2* g) {
 // Supported lengths and their (P, Q) split.  X(N, P, Q)
 #define SR_FFT_SIZES(X)                                                          \
   X(1, 1, 1) X(2, 1, 2) X(3, 1, 3) X(4, 1, 4) X(5, 1, 5) X(6, 1, 6) X(8, 1, 8)             \
-  X(10, 1, 10) X(12, 1, 12) X(16, 1, 16) X(20, 1, 20) X(24, 1, 24) X(25, 1, 25) \
-  X(32, 16, 2) X(40, 8, 5) X(48, 16, 3) X(50, 10, 5) X(64, 16, 4)              \
-  X(80, 16, 5) X(96, 16, 6) X(100, 10, 10) X(128, 16, 8) X(160, 16, 10)         \
-  X(192, 16, 12) X(200, 20, 10) X(256, 16, 16) X(320, 20, 16) X(384, 24, 16)    \
-  X(400, 20, 20) X(512, 32, 16) X(640, 32, 20) X(768, 32, 24) X(800, 32, 25)    \
-  X(1024, 32, 32)
+  X(9, 1, 9) X(10, 1, 10) X(12, 1, 12) X(15, 1, 15) X(16, 1, 16) X(18, 1, 18)   \
+  X(20, 1, 20) X(24, 1, 24) X(25, 1, 25) X(30, 1, 30)                          \
+  X(32, 16, 2) X(36, 12, 3) X(40, 8, 5) X(48, 16, 3) X(50, 10, 5) X(60, 12, 5)  \
+  X(64, 16, 4) X(72, 12, 6) X(80, 16, 5) X(90, 10, 9) X(96, 16, 6)             \
+  X(100, 10, 10) X(120, 12, 10) X(128, 16, 8) X(144, 12, 12) X(150, 25, 6)     \
+  X(160, 16, 10) X(180, 20, 9) X(192, 16, 12) X(200, 20, 10) X(240, 20, 12)    \
+  X(250, 25, 10) X(256, 16, 16) X(270, 30, 9) X(288, 24, 12) X(300, 20, 15)    \
+  X(320, 20, 16) X(360, 24, 15) X(384, 24, 16) X(400, 20, 20) X(450, 30, 15)   \
+  X(480, 24, 20) X(500, 25, 20) X(512, 32, 16) X(540, 30, 18) X(576, 24, 24)   \
+  X(600, 24, 25) X(640, 32, 20) X(720, 30, 24) X(750, 30, 25) X(768, 32, 24)   \
+  X(800, 32, 25) X(900, 30, 30) X(960, 32, 30) X(1024, 32, 32)

@@ -1,0 +1,24 @@
+// Size bucket SR_BUCKET_ID of the per-axis NUFFT FFT kernels (see fft_axis.cuh); the
+// generated wrappers fft_axis_inst_<k>.cu define SR_BUCKET_ID / SR_BUCKET_SIZES.
+#include "fft_axis.cuh"
+
+#define SR_CAT2(a, b) a##b
+#define SR_CAT(a, b) SR_CAT2(a, b)
+
+int SR_CAT(sr_fft_axis_b, SR_BUCKET_ID)(float2* data, long long outer, int n, long long inner, int inv,
+                                       cudaStream_t st) {
+  if (inner == 1) {
+    switch (n) {
+#define X(N_, P_, Q_) case N_: return launch_rows<P_, Q_>(data, outer, inv, st);
+      SR_BUCKET_SIZES(X)
+#undef X
+      default: return SR_EUNSUPPORTED;
+    }
+  }
+  switch (n) {
+#define X(N_, P_, Q_) case N_: return launch_strided<P_, Q_>(data, outer, inner, inv, st);
+    SR_BUCKET_SIZES(X)
+#undef X
+    default: return SR_EUNSUPPORTED;
+  }
+}

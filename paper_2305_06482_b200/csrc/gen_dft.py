@@ -20,7 +20,7 @@ import math
 import sys
 from pathlib import Path
 
-SIZES = (1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 25, 32)
+SIZES = (1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 30, 32)
 
 
 def _fmt(v: float) -> str:
@@ -237,6 +237,41 @@ def generate_twiddles() -> str:
     return "\n".join(parts)
 
 
+CART_BUCKETS = 6
+
+
+def generate_buckets() -> tuple[str, dict[str, str]]:
+    """Split SR_FFT_SIZES into CART_BUCKETS round-robin lists (largest sizes first) so the
+    Cartesian kernels of each list compile in their own translation unit."""
+    sizes = sorted(fft_sizes(), key=lambda t: -t[0])
+    buckets = [[] for _ in range(CART_BUCKETS)]
+    for i, t in enumerate(sizes):
+        buckets[i % CART_BUCKETS].append(t)
+    lines = ["// AUTO-GENERATED by gen_dft.py -- do not edit.",
+             "// Size buckets of the Cartesian kernel instantiations (one translation unit each).",
+             "#pragma once", ""]
+    lines.append("#define SR_CART_BUCKETS(X) " + " ".join(f"X({k})" for k in range(CART_BUCKETS)))
+    for k, b in enumerate(buckets):
+        lines.append(f"#define SR_FFT_SIZES_B{k}(X) " + " ".join(f"X({n}, {p}, {q})" for n, p, q in sorted(b)))
+    wrappers = {}
+    for k in range(CART_BUCKETS):
+        wrappers[f"fft_axis_inst_{k}.cu"] = (
+            "// AUTO-GENERATED by gen_dft.py -- do not edit.\n"
+            f"// NUFFT per-axis FFT kernels, size bucket {k} (see fft_axis_inst.cuh).\n"
+            '#include "fft_buckets_gen.cuh"\n'
+            f"#define SR_BUCKET_ID {k}\n"
+            f"#define SR_BUCKET_SIZES SR_FFT_SIZES_B{k}\n"
+            '#include "fft_axis_inst.cuh"\n')
+        wrappers[f"cart_inst_{k}.cu"] = (
+            "// AUTO-GENERATED by gen_dft.py -- do not edit.\n"
+            f"// Cartesian kernels, size bucket {k} (see cart_inst.cuh).\n"
+            '#include "fft_buckets_gen.cuh"\n'
+            f"#define SR_BUCKET_ID {k}\n"
+            f"#define SR_BUCKET_SIZES SR_FFT_SIZES_B{k}\n"
+            '#include "cart_inst.cuh"\n')
+    return "\n".join(lines) + "\n", wrappers
+
+
 def _write(out: Path, text: str) -> None:
     if not out.exists() or out.read_text() != text:
         out.write_text(text)
@@ -246,6 +281,10 @@ def main(argv):
     out = Path(argv[1]) if len(argv) > 1 else Path(__file__).with_name("dft_gen.cuh")
     _write(out, generate())
     _write(out.with_name("tw_gen.cuh"), generate_twiddles())
+    hdr, wrappers = generate_buckets()
+    _write(out.with_name("fft_buckets_gen.cuh"), hdr)
+    for name, text in wrappers.items():
+        _write(out.with_name(name), text)
 
 
 if __name__ == "__main__":
