@@ -80,7 +80,8 @@ def test_wavelet_and_prox(cuda, name):
     assert abs(reg.value(g["x"]) - float(g["value"])) < 1e-5 * float(g["value"])
 
 
-@pytest.mark.parametrize("dims", [(320, 320), (256, 256), (256, 160), (64, 64), (64, 40), (200, 80)])
+@pytest.mark.parametrize("dims", [(320, 320), (256, 256), (256, 160), (64, 64), (64, 40), (200, 80), (240, 180),
+                                  (90, 150), (36, 30)])
 def test_batched_normal_op_vs_oracle(cuda, dims):
     """K1 at BASELINE geometries (a few slices, per-slice masks and maps)."""
     from paper_2305_06482_b200.cartesian import CartesianKernel
