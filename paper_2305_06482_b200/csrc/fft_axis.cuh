@@ -3,6 +3,56 @@
 #pragma once
 #include "fft2step.cuh"
 
+// Zero-padding structure of an oversampled NUFFT axis of length g holding an image axis of
+// length n (centered: image index i sits at grid index (i - n/2) mod g, linops.py:438-446).
+static __device__ __forceinline__ bool ax_inside(int k, int n, int g) {
+  const int h = n >> 1;
+  return k < n - h || k >= g - h;
+}
+static __device__ __forceinline__ int ax_wrap(int i, int n, int g) {
+  const int r = i - (n >> 1);
+  return r < 0 ? r + g : r;
+}
+
+// Pruning of one strided FFT pass: inputs outside the image extent nin are zero (forward
+// passes over a zero-padded axis), outputs outside nout are not needed (inverse passes before
+// a crop), and of the outer planes only the on (of og) image planes are live.
+struct AxPrune {
+  int nin, nout;  // extents along the FFT axis (== N: no pruning)
+  int on, og;     // live / total planes of the axis just outside (on == og: all planes)
+  __device__ __forceinline__ bool in(int k, int N) const { return nin == N || ax_inside(k, nin, N); }
+  __device__ __forceinline__ bool out(int k, int N) const { return nout == N || ax_inside(k, nout, N); }
+  __device__ __forceinline__ long long plane(long long o) const {
+    if (on == og) return o;
+    const long long j = o / on;
+    return j * og + ax_wrap((int)(o - j * on), on, og);
+  }
+};
+
+// ----------------------------------------------------------------- fused NUFFT row passes
+// The first forward FFT pass (contiguous axis 2) fused with the embed (c_j (x - a) / apod
+// into the zero-padded grid), and the last inverse pass fused with the crop, the conjugate
+// coil sum and the solver epilogue.  Only rows whose (k0, k1) lie inside the image are
+// touched: the strided passes treat the others as zero (AxPrune).
+struct RowGeom {
+  const float2* x;
+  const float2* anchor;
+  const float2* maps;
+  const float* ia0;
+  const float* ia1;
+  const float* ia2;
+  float2* grid;
+  float2* out;
+  int n0, n1, n2, g0, g1, g2;
+  long long D, G;
+  int ncoils;
+  float scale;
+  const float4* coef;
+  const float2* u;
+  const float2* d;
+};
+
+
 namespace {
 
 // ----------------------------------------------------------------- FFT along an axis
@@ -90,10 +140,14 @@ k_fft_rows(float2* __restrict__ data, long long nrows, int inv) {
   }
 }
 
-// strided axis of [outer][N][inner]: CTA = CB consecutive inner indices of one outer
+// strided axis of [outer][N][inner]: CTA = CB consecutive inner indices of PLANES outer
+// planes, walked in turn.  Forward: step 1 reads the natural-order column strip from global
+// (coil/plane p+1's strip is prefetched into registers while plane p transforms), step 2 writes
+// its perm-order groups straight to global.  Inverse: step 2' reads its perm-order group from
+// global, step 1' writes natural order.  One shared-memory exchange per plane either way.
 template <int P, int Q>
 __global__ void __launch_bounds__(AxCfg<P, Q>::TS)
-k_fft_strided(float2* __restrict__ data, long long inner, int inv) {
+k_fft_strided(float2* __restrict__ data, long long inner, int inv, AxPrune pr, int nplanes, int planes) {
   using S = FftShape<P, Q>;
   using A = AxCfg<P, Q>;
   constexpr int N = S::N, CB = A::CB, T = A::TS, VSP = A::VSP;
@@ -102,62 +156,75 @@ k_fft_strided(float2* __restrict__ data, long long inner, int inv) {
   float2* buf = dsm + N;
   const int tid = threadIdx.x;
   const long long c0 = (long long)blockIdx.x * CB;
-  const long long o = blockIdx.y;
-  float2* img = data + o * N * inner;
   const int ncols = (int)min((long long)CB, inner - c0);
   const int c = tid % CB, p = tid / CB;
   const bool cvalid = c < ncols;
+  const long long step = (long long)P * inner;  // distance between q and q+1 along the axis
+  const int o0 = blockIdx.y * planes, o1 = min(nplanes, o0 + planes);
   if (inv) init_tw_s2<P, Q>(tw, tid, T); else init_tw_s1<P, Q>(tw, tid, T);
-  __syncthreads();
   if (!inv) {
-    float2 r[Q];
+    // this thread's natural positions p + P q; pruned inputs are zero
+    float2 rn[Q];
+    auto fetch = [&](int o) {
+      const float2* col = data + pr.plane(o) * N * inner + (long long)p * inner + c0 + c;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) r[q] = cvalid ? img[(long long)(p + P * q) * inner + c0 + c] : make_float2(0.f, 0.f);
-    fft_s1_fwd<P, Q>(r, p, tw);
-#pragma unroll
-    for (int k2 = 0; k2 < Q; ++k2) buf[c * VSP + S::GS * k2 + p] = r[k2];
+      for (int q = 0; q < Q; ++q)
+        rn[q] = (cvalid && pr.in(p + P * q, N)) ? __ldcg(col + q * step) : make_float2(0.f, 0.f);
+    };
+    fetch(o0);
     __syncthreads();
-    for (int it = tid; it < CB * Q; it += T) {
-      const int cc = it % CB, k2 = it / CB;
-      if (cc >= ncols || P == 1) continue;
-      float2 g[P];
-      float2* gp = buf + cc * VSP + S::GS * k2;
+    for (int o = o0; o < o1; ++o) {
+      float2* img = data + pr.plane(o) * N * inner;
+      float2 r[Q];
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-      fft_s2_fwd<P>(g);
+      for (int q = 0; q < Q; ++q) r[q] = rn[q];
+      if (o + 1 < o1) fetch(o + 1);
+      fft_s1_fwd<P, Q>(r, p, tw);
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
-    }
-    __syncthreads();
-    for (int e = tid; e < CB * N; e += T) {
-      const int cc = e % CB, pos = e / CB;
-      if (cc < ncols) img[(long long)pos * inner + c0 + cc] = buf[cc * VSP + S::pad(pos)];
+      for (int k2 = 0; k2 < Q; ++k2) buf[c * VSP + S::GS * k2 + p] = r[k2];
+      __syncthreads();
+      for (int it = tid; it < CB * Q; it += T) {
+        const int cc = it % CB, k2 = it / CB;
+        if (cc >= ncols) continue;
+        float2 g[P];
+        const float2* gp = buf + cc * VSP + S::GS * k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+        if (P > 1) fft_s2_fwd<P>(g);
+        float2* dst = img + (long long)(P * k2) * inner + c0 + cc;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) dst[(long long)k1 * inner] = g[k1];
+      }
+      __syncthreads();  // buf is rewritten by the next plane
     }
   } else {
-    for (int e = tid; e < CB * N; e += T) {
-      const int cc = e % CB, pos = e / CB;
-      if (cc < ncols) buf[cc * VSP + S::pad(pos)] = img[(long long)pos * inner + c0 + cc];
-    }
     __syncthreads();
-    for (int it = tid; it < CB * Q; it += T) {
-      const int cc = it % CB, k2 = it / CB;
-      if (cc >= ncols || P == 1) continue;
-      float2 g[P];
-      float2* gp = buf + cc * VSP + S::GS * k2;
+    for (int o = o0; o < o1; ++o) {
+      float2* img = data + pr.plane(o) * N * inner;
+      for (int it = tid; it < CB * Q; it += T) {
+        const int cc = it % CB, k2 = it / CB;
+        if (cc >= ncols) continue;
+        float2 g[P];
+        const float2* src = img + (long long)(P * k2) * inner + c0 + cc;
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-      fft_s2_inv<P, Q>(g, k2, tw);
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = __ldcg(src + (long long)k1 * inner);
+        if (P > 1) fft_s2_inv<P, Q>(g, k2, tw);
+        float2* gp = buf + cc * VSP + S::GS * k2;
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
-    }
-    __syncthreads();
-    float2 r[Q];
+        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      }
+      __syncthreads();
+      float2 r[Q];
 #pragma unroll
-    for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[c * VSP + S::GS * k2 + p];
-    fft_s1_inv<Q>(r);
-    if (cvalid) {
+      for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[c * VSP + S::GS * k2 + p];
+      fft_s1_inv<Q>(r);
+      if (cvalid) {
+        float2* col = img + (long long)p * inner + c0 + c;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) img[(long long)(p + P * q) * inner + c0 + c] = r[q];
+        for (int q = 0; q < Q; ++q)
+          if (pr.out(p + P * q, N)) col[q * step] = r[q];
+      }
+      __syncthreads();
     }
   }
 }
@@ -181,7 +248,8 @@ int launch_rows(float2* data, long long nrows, int inv, cudaStream_t st) {
 }
 
 template <int P, int Q>
-int launch_strided(float2* data, long long outer, long long inner, int inv, cudaStream_t st) {
+int launch_strided(float2* data, long long outer, long long inner, int inv, cudaStream_t st,
+                   AxPrune pr = AxPrune{P * Q, P * Q, 1, 1}) {
   using A = AxCfg<P, Q>;
   using S = FftShape<P, Q>;
   const size_t smem = sizeof(float2) * (S::N + A::CB * A::VSP);
@@ -191,9 +259,200 @@ int launch_strided(float2* data, long long outer, long long inner, int inv, cuda
       return SR_ECUDA;
     cfg = true;
   }
-  if (outer > 65535) return SR_EINVAL;
-  dim3 grid((unsigned)((inner + A::CB - 1) / A::CB), (unsigned)outer);
-  k_fft_strided<P, Q><<<grid, A::TS, smem, st>>>(data, inner, inv);
+  // planes per CTA: enough column strips to fill the GPU ~4 times, the rest walked in turn
+  const long long strips = (inner + A::CB - 1) / A::CB;
+  const long long target = 148LL * 16;
+  int planes = (int)((strips * outer + target - 1) / target);
+  planes = planes < 1 ? 1 : (planes > 8 ? 8 : planes);
+  const long long gy = (outer + planes - 1) / planes;
+  if (gy > 65535) return SR_EINVAL;
+  dim3 grid((unsigned)strips, (unsigned)gy);
+  k_fft_strided<P, Q><<<grid, A::TS, smem, st>>>(data, inner, inv, pr, (int)outer, planes);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(AxCfg<P, Q>::T)
+k_embed_rows(const RowGeom rg) {
+  using S = FftShape<P, Q>;
+  using A = AxCfg<P, Q>;
+  constexpr int N = S::N, ROWS = A::ROWS, T = A::T;
+  extern __shared__ __align__(16) float2 dsm[];
+  __shared__ long long rbase[ROWS];
+  float2* tw = dsm;
+  float2* buf = dsm + N;
+  const int tid = threadIdx.x;
+  const long long nrows = (long long)rg.ncoils * rg.n0 * rg.n1;
+  const long long row0 = (long long)blockIdx.x * ROWS;
+  const int lr = tid / P, p = tid % P;
+  init_tw_s1<P, Q>(tw, tid, T);
+  const long long rid = row0 + lr;
+  const bool valid = rid < nrows;
+  const long long plane = (long long)rg.n0 * rg.n1;
+  const int j = valid ? (int)(rid / plane) : 0;
+  const long long rem = valid ? rid - (long long)j * plane : 0;
+  const int i0 = (int)(rem / rg.n1), i1 = (int)(rem - (long long)i0 * rg.n1);
+  if (p == 0)
+    rbase[lr] = (long long)j * rg.G +
+                ((long long)ax_wrap(i0, rg.n0, rg.g0) * rg.g1 + ax_wrap(i1, rg.n1, rg.g1)) * N;
+  const long long pixrow = ((long long)i0 * rg.n1 + i1) * rg.n2;
+  const float s01 = valid ? rg.ia0[i0] * rg.ia1[i1] : 0.f;
+  const float2* mj = rg.maps + (long long)j * rg.D + pixrow;
+  const float2* xr = rg.x + pixrow;
+  const float2* ar = rg.anchor ? rg.anchor + pixrow : xr;  // never null-based
+  const int h2 = rg.n2 >> 1;
+  float2 r[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k2 = p + P * q;
+    float2 v = make_float2(0.f, 0.f);
+    if (valid && ax_inside(k2, rg.n2, N)) {
+      const int i2 = (k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2;
+      float2 xv = xr[i2];
+      if (rg.anchor) xv = csub(xv, ar[i2]);
+      v = cscale(cmul(mj[i2], xv), s01 * rg.ia2[i2]);
+    }
+    r[q] = v;
+  }
+  __syncthreads();
+  fft_s1_fwd<P, Q>(r, p, tw);
+#pragma unroll
+  for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
+  __syncthreads();
+  if (P > 1) {
+    for (int it = tid; it < ROWS * Q; it += T) {
+      const int l2 = it / Q, k2 = it - l2 * Q;
+      float2 g[P];
+      float2* gp = buf + l2 * S::VS + S::GS * k2;
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+      fft_s2_fwd<P>(g);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+    }
+    __syncthreads();
+  }
+  const int nv = (int)min((long long)ROWS, nrows - row0);
+  for (int e = tid; e < nv * N; e += T) {
+    const int l3 = e / N, pos = e - l3 * N;
+    rg.grid[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(pos)];
+  }
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(AxCfg<P, Q>::T)
+k_rows_crop(const RowGeom rg) {
+  using S = FftShape<P, Q>;
+  using A = AxCfg<P, Q>;
+  constexpr int N = S::N, ROWS = A::ROWS, T = A::T;
+  constexpr int TILE = ROWS * S::VS;
+  extern __shared__ __align__(16) float2 dsm[];
+  __shared__ long long rbase[ROWS];
+  float2* tw = dsm;
+  float2* bufs = dsm + N;  // two row tiles: coil j+1 streams in (cp.async) while coil j transforms
+  const int tid = threadIdx.x;
+  const long long nrows = (long long)rg.n0 * rg.n1;
+  const long long row0 = (long long)blockIdx.x * ROWS;
+  const int lr = tid / P, p = tid % P;
+  init_tw_s2<P, Q>(tw, tid, T);
+  const long long rid = row0 + lr;
+  const bool valid = rid < nrows;
+  const int i0 = valid ? (int)(rid / rg.n1) : 0;
+  const int i1 = valid ? (int)(rid - (long long)i0 * rg.n1) : 0;
+  if (p == 0) rbase[lr] = ((long long)ax_wrap(i0, rg.n0, rg.g0) * rg.g1 + ax_wrap(i1, rg.n1, rg.g1)) * N;
+  const long long pixrow = ((long long)i0 * rg.n1 + i1) * rg.n2;
+  const int h2 = rg.n2 >> 1;
+  const int nv = (int)min((long long)ROWS, nrows - row0);
+  // natural output positions k2 = p + P q of this thread inside the image, and their pixel
+  int i2s[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k2 = p + P * q;
+    i2s[q] = (valid && ax_inside(k2, rg.n2, N)) ? ((k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2) : -1;
+  }
+  float2 acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = make_float2(0.f, 0.f);
+  __syncthreads();  // rbase
+  auto issue = [&](int j) {
+    const float2* gj = rg.grid + (long long)j * rg.G;
+    float2* dst = bufs + (j & 1) * TILE;
+    for (int e = tid; e < nv * N; e += T) {
+      const int l3 = e / N, pos = e - l3 * N;
+      cp_async8(dst + l3 * S::VS + S::pad(pos), gj + rbase[l3] + pos);
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  for (int j = 0; j < rg.ncoils; ++j) {
+    if (j + 1 < rg.ncoils) {
+      issue(j + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    float2 m[Q];
+    const float2* mj = rg.maps + (long long)j * rg.D + pixrow;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) m[q] = (i2s[q] >= 0) ? mj[i2s[q]] : make_float2(0.f, 0.f);
+    __syncthreads();
+    float2* buf = bufs + (j & 1) * TILE;
+    if (P > 1) {
+      for (int it = tid; it < ROWS * Q; it += T) {
+        const int l2 = it / Q, k2 = it - l2 * Q;
+        float2 g[P];
+        float2* gp = buf + l2 * S::VS + S::GS * k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+        fft_s2_inv<P, Q>(g, k2, tw);
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      }
+      __syncthreads();
+    }
+    float2 r[Q];
+#pragma unroll
+    for (int k2 = 0; k2 < Q; ++k2) r[k2] = buf[lr * S::VS + S::GS * k2 + p];
+    fft_s1_inv<Q>(r);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) cfma_conj(acc[q], m[q], r[q]);
+    __syncthreads();  // buf (j & 1) is refilled by the prefetch issued next iteration
+  }
+  if (!valid) return;
+  const float s01 = rg.ia0[i0] * rg.ia1[i1] * rg.scale;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i2 = i2s[q];
+    if (i2 < 0) continue;
+    const long long pix = pixrow + i2;
+    float2 v = cscale(acc[q], s01 * rg.ia2[i2]);
+    if (rg.coef) {
+      const float4 cf = rg.coef[0];
+      v = cscale(v, cf.x);
+      if (rg.u) { const float2 uu = rg.u[pix]; v.x = fmaf(cf.y, uu.x, v.x); v.y = fmaf(cf.y, uu.y, v.y); }
+      if (rg.d) { const float2 dd = rg.d[pix]; v.x = fmaf(cf.z, dd.x, v.x); v.y = fmaf(cf.z, dd.y, v.y); }
+    }
+    rg.out[pix] = v;
+  }
+}
+
+template <int P, int Q, bool INV>
+int launch_row_fused(const RowGeom& rg, cudaStream_t st) {
+  using A = AxCfg<P, Q>;
+  using S = FftShape<P, Q>;
+  const size_t smem = sizeof(float2) * (S::N + (INV ? 2 : 1) * A::ROWS * S::VS);
+  auto kern = INV ? k_rows_crop<P, Q> : k_embed_rows<P, Q>;
+  static bool cfg = false;
+  if (!cfg) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SR_ECUDA;
+    cfg = true;
+  }
+  const long long nrows = INV ? (long long)rg.n0 * rg.n1 : (long long)rg.ncoils * rg.n0 * rg.n1;
+  const long long nblk = (nrows + A::ROWS - 1) / A::ROWS;
+  if (nblk > 0x7fffffffLL) return SR_EINVAL;
+  kern<<<(unsigned)nblk, A::T, smem, st>>>(rg);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }

@@ -22,3 +22,23 @@ int SR_CAT(sr_fft_axis_b, SR_BUCKET_ID)(float2* data, long long outer, int n, lo
     default: return SR_EUNSUPPORTED;
   }
 }
+
+int SR_CAT(sr_fft_axis_pruned_b, SR_BUCKET_ID)(float2* data, long long outer, int n, long long inner, int inv,
+                                              AxPrune pr, cudaStream_t st) {
+  switch (n) {
+#define X(N_, P_, Q_) case N_: return launch_strided<P_, Q_>(data, outer, inner, inv, st, pr);
+    SR_BUCKET_SIZES(X)
+#undef X
+    default: return SR_EUNSUPPORTED;
+  }
+}
+
+int SR_CAT(sr_nufft_row_fused_b, SR_BUCKET_ID)(const RowGeom& rg, int inv, cudaStream_t st) {
+  switch (rg.g2) {
+#define X(N_, P_, Q_) \
+  case N_: return inv ? launch_row_fused<P_, Q_, true>(rg, st) : launch_row_fused<P_, Q_, false>(rg, st);
+    SR_BUCKET_SIZES(X)
+#undef X
+    default: return SR_EUNSUPPORTED;
+  }
+}
