@@ -1,0 +1,101 @@
+"""GPU edge cases of the operator path: empty and ragged sample sets, a single coil, a zero
+update, unsupported sizes and malformed arguments (errors raised, never a silent fallback)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel
+from oracle import sketch_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-4
+
+
+def _kern(dims, pts_list):
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    return CartesianKernel(dims, [cartesian_plan(dims, p) for p in pts_list])
+
+
+def _c64(a):
+    return torch.from_numpy(np.ascontiguousarray(a).astype(np.complex64)).cuda()
+
+
+def test_empty_and_ragged_masks(cuda):
+    """Slice 0 has no samples (A^H A = 0), slice 1 a handful, slice 2 a dense mask."""
+    rng = np.random.default_rng(4)
+    dims, C = (48, 40), 3
+    D = dims[0] * dims[1]
+    half = np.array([n // 2 for n in dims])
+    pts = [np.zeros((0, 2), dtype=np.int64),
+           np.argwhere(rng.random(dims) < 0.01) - half,
+           np.argwhere(rng.random(dims) < 0.5) - half]
+    kern = _kern(dims, pts)
+    maps = (rng.standard_normal((3, C, D)) + 1j * rng.standard_normal((3, C, D))) / 2
+    x = rng.standard_normal((3, D)) + 1j * rng.standard_normal((3, D))
+    out = torch.full((3, D), float("nan"), dtype=torch.complex64, device="cuda")
+    kern.normal(_c64(maps), _c64(x), out)
+    got = out.cpu().numpy()
+    assert np.all(got[0] == 0)
+    for b in (1, 2):
+        ref = O.Sense(maps[b], O.CartesianKernel(dims, pts[b])).normal(x[b])
+        assert rel(got[b], ref) < OP_TOL
+    y = kern.forward(_c64(maps), _c64(x))
+    assert y.shape[-1] == max(len(p) for p in pts)
+    assert np.all(y[0].cpu().numpy() == 0)
+
+
+def test_single_coil_and_zero_update(cuda):
+    """C = 1, and x == anchor gives exactly the epilogue's d term."""
+    rng = np.random.default_rng(5)
+    dims = (32, 32)
+    D = dims[0] * dims[1]
+    pts = [np.argwhere(rng.random(dims) < 0.3) - 16]
+    kern = _kern(dims, pts)
+    maps = rng.standard_normal((1, 1, D)) + 1j * rng.standard_normal((1, 1, D))
+    x = rng.standard_normal((1, D)) + 1j * rng.standard_normal((1, D))
+    out = torch.empty(1, D, dtype=torch.complex64, device="cuda")
+    kern.normal(_c64(maps), _c64(x), out)
+    ref = O.Sense(maps[0], O.CartesianKernel(dims, pts[0])).normal(x[0])
+    assert rel(out.cpu().numpy()[0], ref) < OP_TOL
+    d = rng.standard_normal((1, D)) + 1j * rng.standard_normal((1, D))
+    coef = torch.tensor([[0.7, 0.0, 1.0, 0.0]], dtype=torch.float32, device="cuda")
+    xt = _c64(x)
+    kern.normal(_c64(maps), xt, out, anchor=xt, coef=coef, d=_c64(d))
+    np.testing.assert_allclose(out.cpu().numpy(), d.astype(np.complex64), rtol=0, atol=0)
+
+
+def test_unsupported_size_and_bad_arguments(cuda):
+    from paper_2305_06482_b200 import _lib
+    assert _lib.lib().sr_fft_size_supported(14) == 0  # 2 x 7: no 7-point codelet
+    with pytest.raises(ValueError):
+        _kern((14, 16), [np.zeros((1, 2), dtype=np.int64)])
+    kern = _kern((32, 32), [np.zeros((1, 2), dtype=np.int64)])
+    x = torch.zeros(1, 1024, dtype=torch.complex64, device="cuda")
+    out = torch.empty_like(x)
+    with pytest.raises(ValueError):  # maps of the wrong length
+        kern.normal(torch.zeros(1, 2, 1000, dtype=torch.complex64, device="cuda"), x, out)
+    with pytest.raises(ValueError):  # wrong dtype
+        kern.normal(torch.zeros(1, 2, 1024, dtype=torch.complex128, device="cuda"), x, out)
+    with pytest.raises(ValueError):  # density weights are not defined for Cartesian masks
+        kern.normal(torch.zeros(1, 2, 1024, dtype=torch.complex64, device="cuda"), x, out,
+                    w=torch.ones(1, device="cuda"))
+    # the C ABI rejects bad shapes itself (no launch)
+    with pytest.raises(ValueError):
+        _lib.call("sr_cart_normal", x.data_ptr(), None, x.data_ptr(), 0, None, 0, out.data_ptr(), None,
+                  0, 1, 32, 32, None, None, None, 0, 0)
+
+
+def test_nufft_without_samples(cuda):
+    """A trajectory with no points: the gridded operator is the zero map."""
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    dims = (32, 32)
+    kern = GriddedKernel(dims, np.zeros((0, 2)), 2.0, 4)
+    D = 32 * 32
+    maps = torch.ones(1, 2, D, dtype=torch.complex64, device="cuda")
+    x = torch.ones(1, D, dtype=torch.complex64, device="cuda")
+    out = torch.full_like(x, float("nan"))
+    kern.normal(maps, x, out)
+    assert torch.all(out == 0)
