@@ -41,6 +41,39 @@ def kb_apodization(r_over_g: np.ndarray, width: int, beta: float) -> np.ndarray:
     return width * out
 
 
+def support_safe_frac(u: np.ndarray, b: np.ndarray, w: int) -> np.ndarray:
+    """fp32 tap offsets t = u - b whose device-side KB support decisions equal the reference's.
+
+    The reference evaluates tap k at d = u - (b + k) in float64 and keeps it iff
+    1 - (2 d / w)^2 > 0 (linops.py:404-410).  The unnormalised kernel jumps from I0(0) = 1 to 0
+    at |d| = w/2, so a sample that lies on a grid line up to 1e-16 (cos(pi/2) in a synthetic
+    trajectory) keeps a tap with weight ~1 in float64 that a plain float32 offset drops.  The
+    device tests |2 (t - k) / w| < 1 in float32 (kb_weight, nufft.cu); where that disagrees with
+    float64 the offset is moved by one float32 ulp towards (or away from) the tap, which changes
+    the other taps' weights by ~1e-7 relative.
+    """
+    u = np.asarray(u, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    t32 = (u - b).astype(np.float32)
+    one, two, wf = np.float32(1.0), np.float32(2.0), np.float32(w)
+    for _ in range(8):
+        moved = False
+        for k in range(w):
+            d64 = u - (b + k)
+            ref = (1.0 - (2.0 * d64 / w) ** 2) > 0
+            dev = np.abs((two * (t32 - np.float32(k))) / wf) < one
+            bad = ref != dev
+            if bad.any():
+                tb = t32[bad]
+                toward = np.where(ref[bad], np.sign(np.float32(k) - tb), np.sign(tb - np.float32(k)))
+                toward = np.where(toward == 0, 1.0, toward).astype(np.float32)
+                t32[bad] = np.nextafter(tb, tb + toward * np.float32(np.inf)).astype(np.float32)
+                moved = True
+        if not moved:
+            return t32
+    raise RuntimeError("could not align float32 KB support decisions with float64")
+
+
 class GriddedKernel:
     """Device NUFFT plan for one image grid (2-D or 3-D)."""
 
@@ -68,14 +101,15 @@ class GriddedKernel:
         self.D = int(np.prod(self.dims))
         self.G = int(np.prod(self.gdims))
         self.nmax = self.n_points
-        # tap bases / offsets per axis in fp64 (linops.py:472-476)
+        # tap bases / offsets per axis in fp64 (linops.py:472-476); the fp32 offsets keep the
+        # reference's fp64 support decisions (see support_safe_frac)
         w = self.width
         bases, fracs = [], []
         for a, (n, g) in enumerate(zip(self.dims, self.gdims)):
             u = pts[:, a] * (g / n)
             b = np.ceil(u - w / 2.0)
             bases.append(b.astype(np.int64))
-            fracs.append(u - b)
+            fracs.append(support_safe_frac(u, b, w))
         # bins: tile of binsize^d grid cells holding each sample's first tap; samples sorted by bin
         self.binsize = int(binsize or (8 if nd == 3 else 16))
         B = self.binsize
@@ -107,7 +141,7 @@ class GriddedKernel:
         frac3 = np.zeros((3, self.n_points), dtype=np.float32)
         for a in range(nd):
             base3[pad + a] = bases[a][order]
-            frac3[pad + a] = fracs[a][order].astype(np.float32)
+            frac3[pad + a] = fracs[a][order]
         dev = dv.require_cuda()
         self.device = dev
         self.base = dv.host_to_dev(base3, torch.int32, dev)

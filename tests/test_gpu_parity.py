@@ -278,6 +278,38 @@ def test_nufft_large_2d_vs_oracle(cuda):
     assert rel(y.cpu().numpy().ravel(), O.Sense(maps, ok, w).forward(x)) < OP_TOL
 
 
+def test_nufft_3d_fused_row_passes_vs_oracle(cuda):
+    """3-D grid large enough (n0 n1 >= 9472 image rows) for the fused embed/row-FFT and
+    row-IFFT/crop/coil-sum kernels and the pruned strided passes, with density weights and the
+    FISTA epilogue, against the oracle."""
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    dims = (96, 128, 32)
+    rng = np.random.default_rng(13)
+    pts = synth.cones_3d(dims, n_readouts=60, n_samples=200)
+    D = int(np.prod(dims))
+    maps = (rng.standard_normal((3, D)) + 1j * rng.standard_normal((3, D))) / 3
+    x = rng.standard_normal(int(np.prod(dims))) + 1j * rng.standard_normal(int(np.prod(dims)))
+    w = O.radial_density_weights(pts)
+    ok = O.GriddedKernel(dims, pts, 1.25, 4)
+    ref = O.Sense(maps, ok, w).normal(x)
+    kern = GriddedKernel(dims, pts, 1.25, 4)
+    assert kern.dims[0] * kern.dims[1] >= 9472
+    md = torch.from_numpy(maps.astype(np.complex64)).cuda().unsqueeze(0)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda().view(1, -1)
+    sw = torch.from_numpy(np.sqrt(w)).cuda()
+    out = torch.empty_like(xd)
+    kern.normal(md, xd, out, w=sw)
+    assert rel(out.cpu().numpy().ravel(), ref) < OP_TOL
+    # epilogue: out = 0.5 N(x - a) + u - 0.25 d
+    a, d = (rng.standard_normal(x.size) + 1j * rng.standard_normal(x.size) for _ in range(2))
+    coef = torch.tensor([[0.5, 1.0, -0.25, 0.0]], dtype=torch.float32, device="cuda")
+    t = lambda v: torch.from_numpy(v.astype(np.complex64)).cuda().view(1, -1)  # noqa: E731
+    kern.normal(md, xd, out, anchor=t(a), coef=coef, u=xd, d=t(d), w=sw)
+    ref2 = 0.5 * O.Sense(maps, ok, w).normal(x - a) + x - 0.25 * d
+    assert rel(out.cpu().numpy().ravel(), ref2) < OP_TOL
+
+
 @pytest.mark.parametrize("name", ["recon_radial", "recon_cones3d"])
 def test_coil_sketching_recon_noncartesian_matches_reference(cuda, name):
     g = golden(name)

@@ -92,3 +92,22 @@ def test_oracle_kernel_parity_small():
     u = rng.standard_normal(192) + 1j * rng.standard_normal(192)
     v = rng.standard_normal(3 * len(pts)) + 1j * rng.standard_normal(3 * len(pts))
     assert abs(np.vdot(v, a.forward(u)) - np.vdot(a.adjoint(v), u)) < 1e-10 * np.linalg.norm(u) * np.linalg.norm(v)
+
+
+def test_support_safe_frac_keeps_float64_decisions():
+    """fp32 KB offsets make the same keep/drop decision per tap as the reference's fp64
+    (linops.py:404-410), including samples on grid lines up to 1e-16."""
+    import numpy as np
+    from paper_2305_06482_b200.nufft import support_safe_frac
+    rng = np.random.default_rng(0)
+    for w in (4, 5, 6):
+        edge = np.array([5e-16, -5e-16, 0.0, 1e-12, -1e-12, 2.0, 2.0 - 4e-16, 3.0 + 1e-15, 0.5, 0.5 + 1e-16])
+        u = np.concatenate([rng.uniform(-40, 40, 20000), edge, edge + 17.0]) * 1.25
+        b = np.ceil(u - w / 2.0)
+        t = support_safe_frac(u, b, w)
+        assert t.dtype == np.float32
+        assert np.max(np.abs(t.astype(np.float64) - (u - b))) < 1e-6
+        for k in range(w):
+            ref = (1.0 - (2.0 * (u - (b + k)) / w) ** 2) > 0
+            dev = np.abs((np.float32(2.0) * (t - np.float32(k))) / np.float32(w)) < np.float32(1.0)
+            assert np.array_equal(ref, dev), (w, k)
