@@ -97,9 +97,35 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
       for (int q = 0; q < Q; ++q) mcur[q] = __ldg(mn + P * q);
     }
     fft_s1_fwd<P, Q>(r, p, t1);
+    float2* wj = wb + j * D;
+    if constexpr (S::VEC) {
+      // the previous coil's bulk stores must have read buf before it is overwritten
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncthreads();
+    }
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
     __syncthreads();
+    if constexpr (S::VEC) {
+      // step 2: each perm-order group (P contiguous values, 16-byte aligned in shared and
+      // global memory) goes to the workspace as one TMA bulk store, no copy-out pass
+      for (int it = tid; it < ROWS * Q; it += T) {
+        const int l2 = it / Q, k2 = it - l2 * Q;
+        float2 g[P];
+        float2* gp = buf + l2 * S::VS + S::GS * k2;
+        lds_group<P, true>(g, gp);
+        fft_s2_fwd<P>(g);
+        sts_group<P, true>(gp, g);
+        if (l2 * N < nvalid) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const unsigned src = (unsigned)__cvta_generic_to_shared(gp);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                       :: "l"(wj + (long long)l2 * N + P * k2), "r"(src), "n"(P * 8) : "memory");
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      continue;
+    }
     if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
         const int l2 = it / Q, k2 = it - l2 * Q;
@@ -111,7 +137,6 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
       }
       __syncthreads();
     }
-    float2* wj = wb + j * D;
     if constexpr (S::VEC) {
       for (int e = 2 * tid; e < nvalid; e += 2 * T) {
         const int l3 = e / N, pos = e - l3 * N;
@@ -125,6 +150,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
     }
     __syncthreads();
   }
+  if constexpr (S::VEC) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------- pass C
