@@ -77,6 +77,10 @@ int sr_group_select(int g);
 /* Tuning of the three-launch schedule: coils per CTA of the column pass (0 = one coil per
  * CTA, the generic kernel; default 4). */
 int sr_cart_tune(int col_jc);
+/* Tuning: the row FFT pass stores its output with TMA bulk copies (bulk = 1), through a
+ * coalesced copy-out pass (0), or picks per size (2, default: bulk for 20-element groups with
+ * Q >= 12, where it measured faster); rows shorter than min_n always use the copy-out. */
+int sr_cart_tune_rows(int bulk, int min_n);
 
 /* Workspace bytes sr_cart_normal needs for these arguments. */
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);

@@ -43,6 +43,7 @@ SIGNATURES = {
     "sr_group_ngroups": [_i, _i],
     "sr_group_select": [_i],
     "sr_cart_tune": [_i],
+    "sr_cart_tune_rows": [_i, _i],
     "sr_fused_config": [_i, _i, _i, _i],
     "sr_fused_stats": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,

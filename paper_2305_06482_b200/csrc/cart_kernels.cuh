@@ -5,6 +5,7 @@
 #include "fft2step.cuh"
 
 extern int sr_g_col_jc;  // coils per CTA of k_colnormal (0 = use k_colpass); cart.cu
+extern int sr_g_row_bulk, sr_g_row_bulk_min_n;  // rowfwd TMA bulk stores (on, min row length); cart.cu
 
 enum { COL_NORMAL = 0, COL_FWD = 1, COL_INV = 2 };
 
@@ -36,7 +37,7 @@ template <int P, int Q>
 __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          const float2* __restrict__ maps, float2* __restrict__ ws,
-         int ncoils, int ny, long long x_bstride, long long map_bstride) {
+         int ncoils, int ny, long long x_bstride, long long map_bstride, int bulk) {
   using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   constexpr int XS = RowCfg<P, Q>::XS;
@@ -98,7 +99,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
     }
     fft_s1_fwd<P, Q>(r, p, t1);
     float2* wj = wb + j * D;
-    if constexpr (S::VEC) {
+    if (S::VEC && bulk) {
       // the previous coil's bulk stores must have read buf before it is overwritten
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncthreads();
@@ -106,7 +107,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
 #pragma unroll
     for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
     __syncthreads();
-    if constexpr (S::VEC) {
+    if (S::VEC && bulk) {
       // step 2: each perm-order group (P contiguous values, 16-byte aligned in shared and
       // global memory) goes to the workspace as one TMA bulk store, no copy-out pass
       for (int it = tid; it < ROWS * Q; it += T) {
@@ -120,7 +121,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const unsigned src = (unsigned)__cvta_generic_to_shared(gp);
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(wj + (long long)l2 * N + P * k2), "r"(src), "n"(P * 8) : "memory");
+                       :: "l"(wj + (long long)l2 * N + P * k2), "r"(src), "r"(P * 8) : "memory");
         }
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -150,7 +151,7 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
     }
     __syncthreads();
   }
-  if constexpr (S::VEC) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (S::VEC && bulk) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------- pass C
@@ -438,6 +439,16 @@ k_colnormal(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long lon
 }
 
 // ---------------------------------------------------------------- dispatch
+// rowfwd output through TMA bulk stores: measured faster only for 20-element groups with
+// Q >= 12 (320^2: 0.705 -> 0.680 ms; 256x160 / 384^2 / 640^2 slower) -> mode 2 (auto) picks
+// those; 0 / 1 force the copy-out pass / the bulk stores (sr_cart_tune_rows)
+template <int P, int Q>
+int row_bulk() {
+  if (P * Q < sr_g_row_bulk_min_n) return 0;
+  if (sr_g_row_bulk == 2) return (P == 20 && Q >= 12) ? 1 : 0;
+  return sr_g_row_bulk;
+}
+
 template <int P, int Q>
 int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, float2* ws,
                   int batch, int ncoils, int ny, long long xbs, long long mbs, cudaStream_t st) {
@@ -450,7 +461,8 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
     configured = true;
   }
   dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
-  k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs);
+  k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs,
+                                                   row_bulk<P, Q>());
   SR_CHECK_LAUNCH();
   return SR_OK;
 }

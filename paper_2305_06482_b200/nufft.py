@@ -54,7 +54,14 @@ def support_safe_frac(u: np.ndarray, b: np.ndarray, w: int) -> np.ndarray:
     """
     u = np.asarray(u, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
-    t32 = (u - b).astype(np.float32)
+    t_all = (u - b).astype(np.float32)
+    # only offsets within a few float32 ulps of a support edge (t - k = +-w/2) can disagree
+    edge = np.abs((u - b) * 2.0 - np.round((u - b) * 2.0)) < 1e-5
+    if not edge.any():
+        return t_all
+    idx = np.flatnonzero(edge)
+    u, b = u[idx], b[idx]
+    t32 = t_all[idx]
     one, two, wf = np.float32(1.0), np.float32(2.0), np.float32(w)
     for _ in range(8):
         moved = False
@@ -70,7 +77,8 @@ def support_safe_frac(u: np.ndarray, b: np.ndarray, w: int) -> np.ndarray:
                 t32[bad] = np.nextafter(tb, tb + toward * np.float32(np.inf)).astype(np.float32)
                 moved = True
         if not moved:
-            return t32
+            t_all[idx] = t32
+            return t_all
     raise RuntimeError("could not align float32 KB support decisions with float64")
 
 

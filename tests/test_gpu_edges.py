@@ -99,3 +99,25 @@ def test_nufft_without_samples(cuda):
     out = torch.full_like(x, float("nan"))
     kern.normal(maps, x, out)
     assert torch.all(out == 0)
+
+
+@pytest.mark.parametrize("dims", [(320, 320), (256, 160), (240, 200)])
+def test_row_pass_store_modes_agree(cuda, dims):
+    """The row FFT pass's TMA bulk stores and its copy-out pass write identical workspaces."""
+    from paper_2305_06482_b200 import _lib
+    rng = np.random.default_rng(8)
+    D = dims[0] * dims[1]
+    half = np.array([n // 2 for n in dims])
+    kern = _kern(dims, [np.argwhere(rng.random(dims) < 0.2) - half for _ in range(2)])
+    maps = _c64((rng.standard_normal((2, 3, D)) + 1j * rng.standard_normal((2, 3, D))) / 2)
+    x = _c64(rng.standard_normal((2, D)) + 1j * rng.standard_normal((2, D)))
+    outs = []
+    try:
+        for mode in (0, 1):
+            _lib.call("sr_cart_tune_rows", mode, 0)
+            o = torch.empty_like(x)
+            kern.normal(maps, x, o)
+            outs.append(o.cpu().numpy())
+    finally:
+        _lib.call("sr_cart_tune_rows", 2, 0)
+    np.testing.assert_array_equal(outs[0], outs[1])
