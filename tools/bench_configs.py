@@ -279,6 +279,12 @@ def run_cfg4(with_oracle: bool, scale: float = 1.0, outer: int = 10, inner: int 
             eng._normal(smaps, xin, out)
             torch.cuda.synchronize()
         print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=15), flush=True)
+    if os.environ.get("SR_PROFILE_RECON") and rank == 0:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+            eng.run(2, inner)
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25), flush=True)
     t0 = time.perf_counter()
     res = eng.run(outer, inner)
     torch.cuda.synchronize()
