@@ -45,6 +45,16 @@ def algorithmic_bytes(nslice=NSLICE, D=NY * NX, chat=CHAT):
     return nslice * 8 * D * (chat + 2) + nslice * D / 8
 
 
+def algorithmic_flops(nslice=NSLICE, D=NY * NX, chat=CHAT):
+    """5 D log2 D per 2-D FFT, one forward and one inverse per sketched coil."""
+    import math
+    return nslice * chat * 2 * 5 * D * math.log2(D)
+
+
+FP32_PEAK_TFLOPS = 74.4  # CUDA-core FP32 at 1965 MHz (148 SM x 128 lanes x 2), SURVEY.md 8(d)
+NOMINAL_HBM_GBS = 8000.0  # the nominal figure north_star quotes
+
+
 def measured_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -373,7 +383,12 @@ def main():
                          "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum per apply "
                                            "(profiles/k1_traffic.json)",
                          "kernel": "K1 fused sketched normal op (rowfwd + colnormal + rowinv launches)",
-                         "algorithmic_bytes_per_apply": bytes_apply, "floors": floors},
+                         "algorithmic_bytes_per_apply": bytes_apply, "floors": floors,
+                         "frac_of_nominal_8tbs": achieved / NOMINAL_HBM_GBS,
+                         "fp32_cobound": {"algorithmic_tflop_per_apply": algorithmic_flops() / 1e12,
+                                          "achieved_tflops": algorithmic_flops() / (t_s / args.steps) / 1e12,
+                                          "peak_tflops": FP32_PEAK_TFLOPS,
+                                          "frac": algorithmic_flops() / (t_s / args.steps) / 1e12 / FP32_PEAK_TFLOPS}},
             "gpu_launches": 3 * args.steps,
             "e2e_gpu_launches_per_step": 3 * 8,
             "clocks": clocks,
