@@ -438,6 +438,63 @@ def power_max_eig(apply, dim: int, iters: int = 30, seed: int = 0) -> float:
     return lam
 
 
+# --------------------------------------------------------------------------
+# total variation (linops.py:717-741) and the PDHG sub-solver (solvers.py:138-149, 315-362)
+
+
+def finite_diff_forward(x: np.ndarray, dims) -> np.ndarray:
+    """Per-axis circular forward differences stacked over axes, D -> ndim*D (linops.py:724-729)."""
+    g = np.asarray(x, dtype=np.complex128).reshape(dims)
+    return np.concatenate([(np.roll(g, -1, axis=a) - g).ravel() for a in range(g.ndim)])
+
+
+def finite_diff_adjoint(y: np.ndarray, dims) -> np.ndarray:
+    """Adjoint: sum_a roll(part_a, +1, a) - part_a (linops.py:731-738)."""
+    d = int(np.prod(dims))
+    acc = np.zeros(dims, dtype=np.complex128)
+    for a in range(len(dims)):
+        part = np.asarray(y[a * d:(a + 1) * d]).reshape(dims)
+        acc += np.roll(part, 1, axis=a) - part
+    return acc.ravel()
+
+
+def tv_norm_value(x: np.ndarray, dims, lam: float) -> float:
+    """lam ||D x||_1, complex magnitudes (solvers.py:61-69 with FiniteDiffOp)."""
+    if lam == 0.0:
+        return 0.0
+    return lam * float(np.sum(np.abs(finite_diff_forward(x, dims))))
+
+
+def clamp_magnitude(p: np.ndarray, radius: float) -> np.ndarray:
+    """Project every complex entry onto the disc of the given radius (solvers.py:138-142)."""
+    mag = np.abs(p)
+    factor = np.where(mag > radius, radius / np.where(mag > 0, mag, 1.0), 1.0)
+    return p * factor
+
+
+def pdhg_tv(normal_s, dvec: np.ndarray, anchor: np.ndarray, dims, lam: float, iters: int,
+            cg_iters: int, ratio: float = 1.0, step_scale: float = 0.9) -> np.ndarray:
+    """Chambolle-Pock on min_x 0.5||A_s(x - a)||^2 + Re<d, x> + lam||D x||_1, K = D
+    (coil_sketch.py:200-216 over solvers.py:315-362); ||D|| = 2 sqrt(ndim) (solvers.py:145-148);
+    the data prox solves (A_s^H A_s + I/tau) w = -d - A_s^H A_s (v - a) by cg_iters CG steps."""
+    norm_k = 2.0 * math.sqrt(len(dims))
+    r = math.sqrt(ratio)
+    sigma = r / norm_k * step_scale
+    tau = 1.0 / (r * norm_k) * step_scale
+    x = np.array(anchor, dtype=np.complex128)
+    z = x.copy()
+    p = np.zeros(len(dims) * x.size, dtype=np.complex128)
+    for _ in range(iters):
+        p = clamp_magnitude(p + sigma * finite_diff_forward(z, dims), lam)
+        v = x - tau * finite_diff_adjoint(p, dims)
+        rhs = -dvec - normal_s(v - anchor)
+        w = cg(lambda u: normal_s(u) + u / tau, rhs, np.zeros_like(v), cg_iters)
+        x_new = v + w
+        z = 2.0 * x_new - x
+        x = x_new
+    return x
+
+
 def power_start_vector(dim: int, seed: int = 0) -> np.ndarray:
     g = seed_stream(seed, 0)
     v = g.standard_normal(dim) + 1j * g.standard_normal(dim)
@@ -502,11 +559,13 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
                          c_hat0: int, v: int, s: int, lam: float, outer: int, inner: int,
                          seed: int = 0, weights=None, rademacher_scale: float = 1.0,
                          solver: str = "fista", reg: str = "l1-wavelet",
-                         step_scale: float = 0.9, distribution: str = "rademacher") -> ReconResult:
+                         step_scale: float = 0.9, distribution: str = "rademacher",
+                         cg_iters: int = 8, pdhg_ratio: float = 1.0) -> ReconResult:
     """Outer true-gradient + fresh sketch + warm-started inner solve (coil_sketch.py:220-306).
 
     make_kernel() builds the Fourier kernel (shared by full and sketched ops).
-    reg: 'l1-wavelet' (FISTA) or 'l2' (CG, coil_sketch.py:182-191).
+    reg: 'l1-wavelet' (FISTA), 'l2' (CG, coil_sketch.py:182-191) or 'l1-tv' (PDHG with an
+    inner CG of cg_iters steps, coil_sketch.py:200-216).
     """
     d0, m0, _, _ = coil_compress_svd(data, maps, c_hat0)
     counter = Counter()
@@ -518,6 +577,8 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
     def reg_value(x):
         if reg == "l2":
             return 0.5 * lam * float(np.linalg.norm(x) ** 2) if lam else 0.0
+        if reg == "l1-tv":
+            return tv_norm_value(x, dims, lam)
         return wavelet_l1(x, dims, lam)
 
     def objective(x):
@@ -559,6 +620,8 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
             b = -dvec - lam * anchor
             delta = cg(lambda u: normal_s(u) + lam * u, b, np.zeros(D, dtype=np.complex128), inner)
             x = anchor + delta
+        elif solver == "pdhg":
+            x = pdhg_tv(normal_s, dvec, anchor, dims, lam, inner, cg_iters, pdhg_ratio, step_scale)
         else:
             raise ValueError(solver)
         finite = bool(np.all(np.isfinite(x)))

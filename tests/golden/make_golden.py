@@ -3,7 +3,10 @@
 
 Run in the build container (the only place /root/reference exists):
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [fixture names ...]
+
+(with names, only those fixtures are rewritten; all fixtures are always computed, in order,
+so the shared RNG stream and therefore every fixture stays the same)
 
 Every fixture stores the seeded inputs and the reference outputs (complex128)
 in tests/golden/<name>.npz.  The oracle (oracle/sketch_oracle.py) is pinned
@@ -272,9 +275,24 @@ def main():
                                 diverged=np.array(rep.diverged), weights=weights.w,
                                 oversamp=np.array(1.25), width=np.array(4))
 
+    # --- TV / PDHG sub-solver (appended last: earlier fixtures keep their RNG stream)
+    recon_case("recon_cart_tv", (24, 20), 6, 6, 2, 2, 2e-3, 2, 3, 1.0, solver="pdhg", kind="l1-tv")
+    tv_shape = lo.GridShape((12, 10))
+    xx = crandn(g, tv_shape.size)
+    fd = lo.FiniteDiffOp(tv_shape)
+    yy = crandn(g, fd.out_dim)
+    out["tv_ops"] = dict(dims=np.array((12, 10)), x=xx, y=yy, fwd=fd.forward(xx), adj=fd.adjoint(yy),
+                         clamp=so._clamp_magnitude(yy, 0.8),
+                         value=np.array(so.make_regularizer("l1-tv", 0.3, tv_shape).value(xx)))
+
+    only = set(sys.argv[1:])
+    written = []
     for k, v in out.items():
+        if only and k not in only:
+            continue
         np.savez_compressed(OUT / f"{k}.npz", **v)
-    print("wrote", ", ".join(sorted(out)))
+        written.append(k)
+    print("wrote", ", ".join(sorted(written)))
 
 
 if __name__ == "__main__":

@@ -100,6 +100,7 @@ def _kernel_for(g):
 @pytest.mark.parametrize("name,solver,reg", [("recon_cart", "fista", "l1-wavelet"),
                                              ("recon_cart_pm1", "fista", "l1-wavelet"),
                                              ("recon_cart_cg", "cg", "l2"),
+                                             ("recon_cart_tv", "pdhg", "l1-tv"),
                                              ("recon_radial", "fista", "l1-wavelet"),
                                              ("recon_cones3d", "fista", "l1-wavelet")])
 def test_recon_end_to_end(name, solver, reg):
@@ -114,3 +115,12 @@ def test_recon_end_to_end(name, solver, reg):
     np.testing.assert_allclose(res.objectives, g["objectives"], rtol=1e-9)
     assert res.counts["coil_transform"] == int(g["counts"]) == int(g["expected"])
     assert res.diverged == bool(g["diverged"])
+
+
+def test_tv_operators():
+    g = golden("tv_ops")
+    dims = tuple(int(n) for n in g["dims"])
+    assert rel(O.finite_diff_forward(g["x"], dims), g["fwd"]) < 1e-13
+    assert rel(O.finite_diff_adjoint(g["y"], dims), g["adj"]) < 1e-13
+    assert rel(O.clamp_magnitude(g["y"], 0.8), g["clamp"]) < 1e-14
+    assert abs(O.tv_norm_value(g["x"], dims, 0.3) - float(g["value"])) < 1e-12 * float(g["value"])
