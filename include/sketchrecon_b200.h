@@ -159,6 +159,18 @@ int sr_reduce(int mode, const sr_c64* a, const sr_c64* b, long long n, long long
               int batch, double* partial, double* result, void* stream);
 int sr_reduce_nparts(void);
 
+/* Total variation for the PDHG sub-solver (l1-tv; coil_sketch.py:200-216, solvers.py:315-362).
+ * Images (batch, dims...) complex64, dual variables (batch, ndim, D) axis-major as the
+ * reference's FiniteDiffOp (linops.py:717-741).  dims: host array of ndim extents.
+ *   sr_tv_dual   mode 0: p = clamp(p + sigma[b] * D z, lam) (_clamp_magnitude, solvers.py:138-142)
+ *                mode 1: p = D z (forward differences, for the objective)
+ *   sr_tv_primal v = x - tau[b] * D^H p
+ * sigma / tau: per-slice device float arrays. */
+int sr_tv_dual(sr_c64* p, const sr_c64* z, const int* dims, int ndim, int mode, const float* sigma, float lam,
+               int batch, void* stream);
+int sr_tv_primal(sr_c64* v, const sr_c64* x, const sr_c64* p, const int* dims, int ndim, const float* tau,
+                 int batch, void* stream);
+
 /* K7 -- out = cx*X + cy*Y + cz*Z with per-slice device coefficients (float4) or
  * host coefficients when coef == NULL (axpy / momentum of solvers.py:223-227,293). */
 int sr_lincomb(sr_c64* out, const sr_c64* X, const sr_c64* Y, const sr_c64* Z,

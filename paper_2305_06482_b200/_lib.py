@@ -35,6 +35,8 @@ SIGNATURES = {
     "sr_reduce": [_i, _vp, _vp, _ll, _ll, _i, _vp, _vp, _vp],
     "sr_reduce_nparts": [],
     "sr_lincomb": [_vp, _vp, _vp, _vp, _vp, _f, _f, _f, _ll, _ll, _i, _vp],
+    "sr_tv_dual": [_vp, _vp, _vp, _i, _i, _vp, _f, _i, _vp],
+    "sr_tv_primal": [_vp, _vp, _vp, _vp, _i, _vp, _i, _vp],
     "sr_scalar_op": [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],

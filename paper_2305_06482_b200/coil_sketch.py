@@ -130,8 +130,6 @@ def classical_sketch_solve(a: SenseOperator, y, sk: SketchMatrix, reg: Regulariz
 
 
 def _reg_kind(reg: Regularizer) -> str:
-    if reg.kind == "l1-tv":
-        raise NotImplementedError("l1-tv / PDHG is outside the sketched-operator hot-path scope")
     return reg.kind
 
 
@@ -152,8 +150,6 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     """
     if cfg.c_hat0 > data.n_coils:
         raise ValueError(f"c_hat0 = {cfg.c_hat0} exceeds the {data.n_coils} available coils")
-    if cfg.solver == "pdhg":
-        raise NotImplementedError("pdhg sub-solver is outside the sketched-operator hot-path scope")
     if not cfg.reuse_step_size:
         raise NotImplementedError("reuse_step_size=False is not implemented on the device path")
     kind = _reg_kind(cfg.reg)
@@ -188,7 +184,8 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     eng = SketchedReconEngine(a.kernel, a.maps_dev, ypad, dims=maps.shape.dims, sketch=cfg.sketch,
                               lam=cfg.reg.lam, reg=kind, solver=cfg.solver,
                               step_scale=solver_cfg.step_scale, sqrt_w=a.sqrt_w_dev,
-                              wavelet_levels=getattr(cfg.reg.transform, "levels", None), counter=a.counter)
+                              wavelet_levels=getattr(cfg.reg.transform, "levels", None), counter=a.counter,
+                              pdhg_ratio=solver_cfg.pdhg_sigma_tau_ratio, cg_iters=solver_cfg.inner_cg_iters)
     ref = None if x_ref is None else dv.c64(x_ref.values).view(1, -1)
     res = eng.run(cfg.outer_iters, cfg.inner_iters, x0=x0_dev, x_ref=ref)
     report = ReconReport(x_final=Image(maps.shape, dv.to_numpy128(res.x[0])), energy_fraction=energy,
@@ -213,7 +210,8 @@ def coil_sketching_recon_batched(kernel, maps0: torch.Tensor, y: torch.Tensor, c
     solver_cfg = solver_cfg or SolverConfig(tol=0.0)
     eng = SketchedReconEngine(kernel, maps0, y, dims=dims, sketch=cfg.sketch, lam=cfg.reg.lam,
                               reg=_reg_kind(cfg.reg), solver=cfg.solver, step_scale=solver_cfg.step_scale,
-                              sqrt_w=sqrt_w, wavelet_levels=getattr(cfg.reg.transform, "levels", None))
+                              sqrt_w=sqrt_w, wavelet_levels=getattr(cfg.reg.transform, "levels", None),
+                              pdhg_ratio=solver_cfg.pdhg_sigma_tau_ratio, cg_iters=solver_cfg.inner_cg_iters)
     return eng.run(cfg.outer_iters, cfg.inner_iters, x0=x0)
 
 

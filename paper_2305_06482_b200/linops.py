@@ -12,6 +12,8 @@ device tensors:
 
 from __future__ import annotations
 
+import ctypes
+
 import contextlib
 from dataclasses import dataclass
 
@@ -19,12 +21,13 @@ import numpy as np
 import torch
 
 from . import _device as dv
+from . import _lib
 from .rng import seed_stream
 from .wavelet import WaveletEngine, default_wavelet_levels
 
 __all__ = [
     "GridShape", "Image", "Trajectory", "CostCounter", "LinOp", "IdentityOp", "DiagonalOp",
-    "ComposeOp", "CenteredFFTOp", "CartesianMaskOp", "WaveletOp", "make_fourier_kernel",
+    "ComposeOp", "CenteredFFTOp", "CartesianMaskOp", "WaveletOp", "FiniteDiffOp", "make_fourier_kernel",
     "default_wavelet_levels", "max_eig_power", "dot_test",
 ]
 
@@ -306,6 +309,31 @@ class WaveletOp(LinOp):
         self.counter.add("wavelet")
         out = torch.empty(1, self.in_dim, dtype=torch.complex64, device=y.device)
         return self.engine.adjoint(y.view(1, -1).contiguous(), out)[0]
+
+
+class FiniteDiffOp(LinOp):
+    """Per-axis circular forward differences stacked over axes, D -> ndim*D (linops.py:717-738),
+    on the device (csrc/tv.cu)."""
+
+    def __init__(self, shape: GridShape, counter: CostCounter | None = None):
+        super().__init__(shape.size, shape.ndim * shape.size, counter)
+        self.shape = shape
+        self._dims = (ctypes.c_int * shape.ndim)(*shape.dims)
+
+    def _forward(self, x):
+        self.counter.add("finite_diff")
+        out = torch.empty(self.out_dim, dtype=torch.complex64, device=x.device)
+        _lib.call("sr_tv_dual", dv.ptr(out), dv.ptr(x), self._dims, self.shape.ndim, 1, None, 0.0, 1, dv.stream())
+        return out
+
+    def _adjoint(self, y):
+        self.counter.add("finite_diff")
+        out = torch.empty(self.in_dim, dtype=torch.complex64, device=y.device)
+        zero = torch.zeros(self.in_dim, dtype=torch.complex64, device=y.device)
+        tau = torch.full((1,), -1.0, dtype=torch.float32, device=y.device)  # out = 0 - (-1) D^H y
+        _lib.call("sr_tv_primal", dv.ptr(out), dv.ptr(zero), dv.ptr(y), self._dims, self.shape.ndim, dv.ptr(tau), 1,
+                  dv.stream())
+        return out
 
 
 def make_fourier_kernel(shape: GridShape, traj: Trajectory, method: str = "auto",

@@ -19,6 +19,8 @@ Counters follow the reference tally per slice: 2*C0 per true gradient,
 
 from __future__ import annotations
 
+import ctypes
+
 import math
 import time
 from dataclasses import dataclass, field
@@ -75,7 +77,8 @@ class SketchedReconEngine:
     def __init__(self, kernel, maps0: torch.Tensor, y: torch.Tensor, *, dims, sketch: SketchConfig,
                  lam: float, reg: str = "l1-wavelet", solver: str = "fista", step_scale: float = 0.9,
                  sqrt_w: torch.Tensor | None = None, wavelet_levels: int | None = None,
-                 counter: CostCounter | None = None, shard=None, use_graph: bool | None = None):
+                 counter: CostCounter | None = None, shard=None, use_graph: bool | None = None,
+                 pdhg_ratio: float = 1.0, cg_iters: int = 8):
         self.kernel = kernel
         self.maps0 = maps0.contiguous()          # (B, C0, D) all compressed coils (sketch input)
         self.B, self.C0, self.D = self.maps0.shape
@@ -98,12 +101,20 @@ class SketchedReconEngine:
         self.dims = tuple(dims)
         self.counter = counter if counter is not None else CostCounter()
         self.dev = self.maps0.device
-        if reg not in ("l1-wavelet", "l2"):
-            raise NotImplementedError(f"regularizer {reg!r} is outside the hot-path scope")
+        if reg not in ("l1-wavelet", "l2", "l1-tv"):
+            raise ValueError(f"unknown regularizer {reg!r}")
         if solver == "cg" and reg != "l2":
             raise ValueError("cg sub-solver requires the l2 regularizer")
-        if solver not in ("fista", "cg"):
-            raise NotImplementedError(f"solver {solver!r} is outside the hot-path scope")
+        if solver == "pdhg" and reg != "l1-tv":
+            raise ValueError("pdhg sub-solver requires the l1-tv regularizer")
+        if solver not in ("fista", "cg", "pdhg"):
+            raise ValueError(f"unknown solver {solver!r}")
+        if reg == "l1-tv" and solver != "pdhg":
+            raise NotImplementedError("l1-tv is solved by the pdhg sub-solver (coil_sketch.py:200-216)")
+        self.pdhg_ratio = float(pdhg_ratio)
+        self.cg_iters = int(cg_iters)
+        self.ndim = len(self.dims)
+        self._cdims = (ctypes.c_int * self.ndim)(*self.dims)
         self.wav = WaveletEngine(self.dims, wavelet_levels, batch=self.B) if reg == "l1-wavelet" else None
         B, D = self.B, self.D
         mk = lambda: torch.zeros(B, D, dtype=torch.complex64, device=self.dev)  # noqa: E731
@@ -112,6 +123,9 @@ class SketchedReconEngine:
         self.partial = torch.zeros(kernel.partial_shape(max(1, self.maps_full.shape[1])), dtype=torch.float64,
                                    device=self.dev)
         self.tmp = mk() if self.shard is not None else None
+        if reg == "l1-tv":  # dual variable and scratch of the PDHG sub-solver
+            self.p = torch.zeros(B, self.ndim * D, dtype=torch.complex64, device=self.dev)
+            self.wbuf, self.rhs, self.xn = mk(), mk(), mk()
         # the inner FISTA loop of every outer iteration launches the same kernels on the same
         # buffers, so it can be captured once as a CUDA graph and replayed (t >= 2).  Capture +
         # instantiation costs ~10 ms, saving ~50 us per inner iteration of launch overhead, so
@@ -163,6 +177,10 @@ class SketchedReconEngine:
         if self.lam != 0.0:
             if self.reg == "l1-wavelet":
                 obj = obj + self.lam * self.wav.l1_norm(x)
+            elif self.reg == "l1-tv":
+                _lib.call("sr_tv_dual", dv.ptr(self.p), dv.ptr(x), self._cdims, self.ndim, 1, None, 0.0, self.B,
+                          dv.stream())
+                obj = obj + self.lam * _abs_sum(self.p)
             else:
                 obj = obj + 0.5 * self.lam * _norm2(x)
         return obj
@@ -242,12 +260,14 @@ class SketchedReconEngine:
         self._graph.replay()
         self.counter.add("coil_transform", 2 * self.chat * inner)
 
-    def _cg(self, smaps, inner: int):
-        """(A_s^H A_s + lam I) delta = -d - lam x^t, x = x^t + delta (coil_sketch.py:182-191)."""
+    def _cg_solve(self, smaps, sol, rhs, shift_coef, iters: int):
+        """sol = `iters` CG steps on (A_s^H A_s + shift I) sol = rhs from sol = 0 (_cg_loop,
+        solvers.py:206-229); shift_coef (B, 4) = {1, shift, 0, 0} is the K1 epilogue of the matvec.
+        A slice whose residual vanishes or whose curvature p^H M p <= 0 stops updating, as the
+        reference's loop breaks (state kept on the device, no host sync)."""
         B, D, st = self.B, self.D, dv.stream()
-        delta = torch.zeros_like(self.x)
-        r = torch.empty_like(self.x)
-        _lincomb(r, self.d, self.anchor, None, -1.0, -self.lam, 0.0, B, D)
+        sol.zero_()
+        r = rhs.clone()
         p = r.clone()
         mp = torch.empty_like(r)
         nparts = _lib.lib().sr_reduce_nparts()
@@ -260,20 +280,62 @@ class SketchedReconEngine:
         _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
         state[:, 0] = rs[:, 0]
         state[:, 1] = (rs[:, 0] > 0).to(torch.float64)  # sqrt(rs) <= 0 stops at once
-        lcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
-        lcoef[:, 0] = 1.0
-        lcoef[:, 1] = self.lam
-        for _ in range(inner):
+        for _ in range(iters):
             self.counter.add("coil_transform", 2 * self.chat)
-            self._normal(smaps, p, mp, coef=lcoef, u=p)
+            self._normal(smaps, p, mp, coef=shift_coef, u=p)
             _lib.call("sr_reduce", 1, dv.ptr(p), dv.ptr(mp), D, D, B, dv.ptr(part), dv.ptr(den), st)
             _lib.call("sr_scalar_op", 1, None, dv.ptr(den), dv.ptr(state), dv.ptr(cA), dv.ptr(cB), None, B, st)
-            _lib.call("sr_lincomb", dv.ptr(delta), dv.ptr(delta), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
+            _lib.call("sr_lincomb", dv.ptr(sol), dv.ptr(sol), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
             _lib.call("sr_lincomb", dv.ptr(r), dv.ptr(r), dv.ptr(mp), None, dv.ptr(cB), 0, 0, 0, D, D, B, st)
             _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
             _lib.call("sr_scalar_op", 2, dv.ptr(rs), None, dv.ptr(state), dv.ptr(cA), None, None, B, st)
             _lib.call("sr_lincomb", dv.ptr(p), dv.ptr(r), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
+        return sol
+
+    def _cg(self, smaps, inner: int):
+        """(A_s^H A_s + lam I) delta = -d - lam x^t, x = x^t + delta (coil_sketch.py:182-191)."""
+        B, D = self.B, self.D
+        delta = torch.zeros_like(self.x)
+        rhs = torch.empty_like(self.x)
+        _lincomb(rhs, self.d, self.anchor, None, -1.0, -self.lam, 0.0, B, D)
+        lcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        lcoef[:, 0] = 1.0
+        lcoef[:, 1] = self.lam
+        self._cg_solve(smaps, delta, rhs, lcoef, inner)
         _lincomb(self.x, self.anchor, delta, None, 1.0, 1.0, 0.0, B, D)
+
+    def _pdhg(self, smaps, inner: int):
+        """Chambolle-Pock on min_x 0.5||A_s(x - x^t)||^2 + Re<d, x> + lam ||D x||_1 with K = D
+        (coil_sketch.py:200-216, solvers.py:315-362): per iteration p = clamp(p + sigma D z, lam),
+        v = x - tau D^H p, x' = v + CG_k((A_s^H A_s + I/tau) w = -d - A_s^H A_s (v - x^t)),
+        z = 2 x' - x.  sigma tau ||D||^2 = step_scale^2 with ||D|| = 2 sqrt(ndim)."""
+        B, D, st = self.B, self.D, dv.stream()
+        norm_k = 2.0 * math.sqrt(self.ndim)
+        ratio = math.sqrt(self.pdhg_ratio)
+        sigma = ratio / norm_k * self.step_scale
+        tau = 1.0 / (ratio * norm_k) * self.step_scale
+        sig_t = torch.full((B,), sigma, dtype=torch.float32, device=self.dev)
+        tau_t = torch.full((B,), tau, dtype=torch.float32, device=self.dev)
+        shift = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        shift[:, 0] = 1.0
+        shift[:, 1] = 1.0 / tau
+        rcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        rcoef[:, 0] = -1.0
+        rcoef[:, 2] = -1.0
+        self.x.copy_(self.anchor)
+        self.z.copy_(self.anchor)
+        self.p.zero_()
+        for _ in range(inner):
+            _lib.call("sr_tv_dual", dv.ptr(self.p), dv.ptr(self.z), self._cdims, self.ndim, 0, dv.ptr(sig_t),
+                      self.lam, B, st)
+            _lib.call("sr_tv_primal", dv.ptr(self.v), dv.ptr(self.x), dv.ptr(self.p), self._cdims, self.ndim,
+                      dv.ptr(tau_t), B, st)
+            self.counter.add("coil_transform", 2 * self.chat)
+            self._normal(smaps, self.v, self.rhs, anchor=self.anchor, coef=rcoef, d=self.d)  # -N(v - a) - d
+            self._cg_solve(smaps, self.wbuf, self.rhs, shift, self.cg_iters)
+            _lincomb(self.xn, self.v, self.wbuf, None, 1.0, 1.0, 0.0, B, D)
+            _lincomb(self.z, self.xn, self.x, None, 2.0, -1.0, 0.0, B, D)
+            self.x, self.xn = self.xn, self.x
 
     # ------------------------------------------------------------ Algorithm 1
     def run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
@@ -319,6 +381,8 @@ class SketchedReconEngine:
                     self._fista_graphed(smaps, inner)
                 else:
                     self._fista(smaps, inner)
+            elif self.solver == "pdhg":
+                self._pdhg(smaps, inner)
             else:
                 self._cg(smaps, inner)
             finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1).cpu().numpy()
@@ -350,6 +414,16 @@ class SketchedReconEngine:
         return EngineResult(x, np.array(objs), obj0, diverged, outer_run,
                             np.full(B, np.nan) if lip is None else lip.cpu().numpy(),
                             self.counter.asdict(), cnts, walls, dists)
+
+
+def _abs_sum(x) -> torch.Tensor:
+    B = x.shape[0]
+    n = x.numel() // B
+    nparts = _lib.lib().sr_reduce_nparts()
+    part = torch.empty(B, nparts, 2, dtype=torch.float64, device=x.device)
+    res = torch.empty(B, 2, dtype=torch.float64, device=x.device)
+    _lib.call("sr_reduce", 2, dv.ptr(x), None, n, n, B, dv.ptr(part), dv.ptr(res), dv.stream())
+    return res[:, 0]
 
 
 def _norm2(x) -> torch.Tensor:

@@ -21,7 +21,7 @@ import torch
 from . import _device as dv
 from . import _lib
 from .forward_model import SenseOperator
-from .linops import GridShape, IdentityOp, Image, LinOp, WaveletOp, max_eig_power
+from .linops import FiniteDiffOp, GridShape, IdentityOp, Image, LinOp, WaveletOp, max_eig_power
 
 __all__ = ["Regularizer", "SolverConfig", "SolveResult", "make_regularizer", "prox_l1", "cg_normal",
            "fista", "reconstruct", "normal_max_eig", "composite_objective", "pdhg", "accproxsgd"]
@@ -41,6 +41,11 @@ def _reduce(mode: int, a: torch.Tensor, b: torch.Tensor | None = None) -> torch.
 
 def dev_norm2(a) -> torch.Tensor:
     return _reduce(0, a.contiguous())[:, 0]
+
+
+def dev_abs_sum(a) -> torch.Tensor:
+    """sum |a_i| per row (complex magnitudes), (B,) float64."""
+    return _reduce(2, a.contiguous())[:, 0]
 
 
 def dev_vdot(a, b) -> torch.Tensor:
@@ -81,7 +86,9 @@ class Regularizer:
             return 0.5 * self.lam * float(dev_norm2(xt.view(1, -1))[0])
         if self.kind == "l1-wavelet":
             return self.lam * float(self.transform.engine.l1_norm(xt.view(1, -1))[0])
-        raise NotImplementedError("l1-tv is outside the sketched-operator hot path")
+        with self.transform.paused_counts():
+            tx = self.transform.forward(xt.reshape(-1))
+        return self.lam * float(dev_abs_sum(tx.view(1, -1))[0])
 
     def prox(self, v, step: float, tv_iters: int = 10):
         """prox_{step g}(v) (solvers.py:71-81); numpy in -> numpy out, tensor -> tensor."""
@@ -95,7 +102,7 @@ class Regularizer:
             out = torch.empty_like(vt)
             self.transform.engine.prox(vt.view(1, -1), out.view(1, -1), hthresh=step * self.lam)
         else:
-            raise NotImplementedError("l1-tv is outside the sketched-operator hot path")
+            out = tv_prox(vt.reshape(1, -1), step * self.lam, self.transform.shape, tv_iters).reshape(vt.shape)
         return dv.to_numpy128(out) if host else out
 
 
@@ -106,8 +113,37 @@ def make_regularizer(kind: str, lam: float, shape: GridShape, wavelet_levels: in
     if kind == "l1-wavelet":
         return Regularizer(kind, lam, WaveletOp(shape, wavelet_levels))
     if kind == "l1-tv":
-        raise NotImplementedError("l1-tv (finite differences + PDHG) is outside the hot-path scope")
+        return Regularizer(kind, lam, FiniteDiffOp(shape))
     raise ValueError(f"unknown regularizer kind {kind!r}")
+
+
+def tv_op_norm(ndim: int) -> float:
+    """||D|| = 2 sqrt(ndim) for circular finite differences (solvers.py:145-148)."""
+    return 2.0 * float(np.sqrt(ndim))
+
+
+def tv_prox(v: torch.Tensor, weight: float, shape: GridShape, iters: int) -> torch.Tensor:
+    """argmin_u 0.5||u - v||^2 + weight ||D u||_1 by the reference's short PDHG loop
+    (_tv_prox, solvers.py:152-164), batched over rows of v (B, D) on the device."""
+    import ctypes
+    B, D = v.shape
+    dims = (ctypes.c_int * shape.ndim)(*shape.dims)
+    sigma = tau = 1.0 / max(tv_op_norm(shape.ndim), 1e-12)
+    st = dv.stream()
+    sig_t = torch.full((B,), sigma, dtype=torch.float32, device=v.device)
+    tau_t = torch.full((B,), tau, dtype=torch.float32, device=v.device)
+    x = v.clone()
+    z = x.clone()
+    t = torch.empty_like(x)
+    p = torch.zeros(B, shape.ndim * D, dtype=torch.complex64, device=v.device)
+    for _ in range(int(iters)):
+        _lib.call("sr_tv_dual", dv.ptr(p), dv.ptr(z), dims, shape.ndim, 0, dv.ptr(sig_t), float(weight), B, st)
+        _lib.call("sr_tv_primal", dv.ptr(t), dv.ptr(x), dv.ptr(p), dims, shape.ndim, dv.ptr(tau_t), B, st)
+        xn = torch.empty_like(x)
+        lincomb(xn, t, v, None, 1.0 / (1.0 + tau), tau / (1.0 + tau), 0.0)
+        lincomb(z, xn, x, None, 2.0, -1.0, 0.0)
+        x = xn
+    return x
 
 
 @dataclass(frozen=True)

@@ -204,7 +204,8 @@ def _recon_inputs(g):
 
 @pytest.mark.parametrize("name,solver,kind", [("recon_cart", "fista", "l1-wavelet"),
                                               ("recon_cart_pm1", "fista", "l1-wavelet"),
-                                              ("recon_cart_cg", "cg", "l2")])
+                                              ("recon_cart_cg", "cg", "l2"),
+                                              ("recon_cart_tv", "pdhg", "l1-tv")])
 def test_coil_sketching_recon_matches_reference(cuda, name, solver, kind):
     g = golden(name)
     cs, fm, lo, sk, so, dims, shape, traj, nufft = _recon_inputs(g)
@@ -222,6 +223,38 @@ def test_coil_sketching_recon_matches_reference(cuda, name, solver, kind):
     np.testing.assert_allclose([r.objective for r in rep.per_outer], g["objectives"], rtol=1e-4)
     assert rep.counts["coil_transform"] == int(g["counts"]) == int(g["expected"])
     assert rep.diverged == bool(g["diverged"])
+
+
+def test_tv_operators_match_reference(cuda):
+    """Finite differences, their adjoint, the dual clamp, the TV value and the TV prox on the
+    device against the reference's (linops.py:717-741, solvers.py:61-69,138-164)."""
+    cs, fm, lo, sk, so = _api()
+    from paper_2305_06482_b200 import _lib
+    g = golden("tv_ops")
+    dims = tuple(int(n) for n in g["dims"])
+    shape = lo.GridShape(dims)
+    t = lambda v: torch.from_numpy(np.ascontiguousarray(v).astype(np.complex64)).cuda()  # noqa: E731
+    fd = lo.FiniteDiffOp(shape)
+    assert rel(fd.forward(g["x"]), g["fwd"]) < OP_TOL
+    assert rel(fd.adjoint(g["y"]), g["adj"]) < OP_TOL
+    p = t(g["y"])
+    z = torch.zeros(shape.size, dtype=torch.complex64, device="cuda")
+    sig = torch.ones(1, dtype=torch.float32, device="cuda")
+    import ctypes
+    _lib.call("sr_tv_dual", p.data_ptr(), z.data_ptr(), (ctypes.c_int * 2)(*dims), 2, 0, sig.data_ptr(), 0.8, 1, 0)
+    torch.cuda.synchronize()
+    assert rel(p.cpu().numpy(), g["clamp"]) < OP_TOL
+    reg = so.make_regularizer("l1-tv", 0.3, shape)
+    assert abs(reg.value(g["x"]) - float(g["value"])) < 1e-4 * float(g["value"])
+    ref_prox = O.finite_diff_forward  # the oracle's TV prox below restates solvers.py:152-164
+    v = g["x"]
+    x, z_, pp = v.copy(), v.copy(), np.zeros(2 * v.size, complex)
+    sg = tau = 1.0 / (2.0 * np.sqrt(2.0))
+    for _ in range(10):
+        pp = O.clamp_magnitude(pp + sg * ref_prox(z_, dims), 0.7 * 0.3)
+        xn = (x - tau * O.finite_diff_adjoint(pp, dims) + tau * v) / (1.0 + tau)
+        z_, x = 2.0 * xn - x, xn
+    assert rel(reg.prox(v, 0.7), x) < OP_TOL
 
 
 # ----------------------------------------------------------------------------- NUFFT (K3/K4)
