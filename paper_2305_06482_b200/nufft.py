@@ -124,9 +124,13 @@ class GriddedKernel:
         bpos = [np.mod(bases[a], g) for a, g in enumerate(self.gdims)]
         nbins = [-(-g // B) for g in self.gdims]
         binid = np.zeros(self.n_points, dtype=np.int64)
+        local = np.zeros(self.n_points, dtype=np.int64)
         for a in range(nd):
             binid = binid * nbins[a] + bpos[a] // B
-        order = np.argsort(binid, kind="stable")
+            local = local * B + bpos[a] % B
+        # within a bin, samples sharing a first-tap cell are adjacent: the spread merges such
+        # runs in registers before its shared atomics (about 3 samples per cell at config 4)
+        order = np.argsort(binid * B ** nd + local, kind="stable")
         self.order = order
         chunks = []
         if self.n_points:

@@ -311,6 +311,39 @@ def test_nufft_large_2d_vs_oracle(cuda):
     assert rel(y.cpu().numpy().ravel(), O.Sense(maps, ok, w).forward(x)) < OP_TOL
 
 
+def test_nufft_3d_dense_centre_runs_vs_oracle(cuda):
+    """Many samples per grid cell (dense cone centre): the spread merges runs of samples that
+    share a first-tap cell in registers before the shared atomics; the normal op, forward and
+    adjoint must still match the oracle."""
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    dims = (24, 24, 16)
+    rng = np.random.default_rng(5)
+    pts = synth.cones_3d(dims, n_readouts=400, n_samples=256)
+    D = int(np.prod(dims))
+    maps = (rng.standard_normal((2, D)) + 1j * rng.standard_normal((2, D))) / 3
+    x = rng.standard_normal(D) + 1j * rng.standard_normal(D)
+    w = O.radial_density_weights(pts)
+    ok = O.GriddedKernel(dims, pts, 1.25, 4)
+    kern = GriddedKernel(dims, pts, 1.25, 4)
+    g = [np.ceil(pts[:, a] * (kern.gdims[a] / dims[a]) - 2.0) for a in range(3)]
+    assert len(pts) / len(np.unique(np.stack(g), axis=1).T) > 4  # long runs
+    md = torch.from_numpy(maps.astype(np.complex64)).cuda().unsqueeze(0)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda().view(1, -1)
+    sw = torch.from_numpy(np.sqrt(w)).cuda()
+    out = torch.empty_like(xd)
+    kern.normal(md, xd, out, w=sw)
+    e_n = rel(out.cpu().numpy().ravel(), O.Sense(maps, ok, w).normal(x))
+    y = kern.forward(md, xd, w=sw)
+    yr = O.Sense(maps, ok, w).forward(x)
+    e_f = rel(y.cpu().numpy().ravel(), yr)
+    adj = torch.empty_like(xd)
+    kern.adjoint(md, torch.from_numpy(yr.astype(np.complex64)).cuda().view(1, 2, -1), adj, w=sw)
+    e_a = rel(adj.cpu().numpy().ravel(), O.Sense(maps, ok, w).adjoint(yr))
+    print(f"dense-centre 3-D: normal {e_n:.2e} forward {e_f:.2e} adjoint {e_a:.2e}")
+    assert max(e_n, e_f, e_a) < OP_TOL
+
+
 def test_nufft_3d_fused_row_passes_vs_oracle(cuda):
     """3-D grid large enough (n0 n1 >= 9472 image rows) for the fused embed/row-FFT and
     row-IFFT/crop/coil-sum kernels and the pruned strided passes, with density weights and the
