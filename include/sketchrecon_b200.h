@@ -214,6 +214,18 @@ int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int*
                      long long nsamples, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
                      const sr_c64* d, const int* chunks, int nchunks, int binsize, void* stream);
 int sr_nufft_partial_blocks(long long nsamples);
+/* NUFFT plan on the device (replaces the host loop of _GriddedNUFFTKernel._build_interpolator,
+ * linops.py:464-492, for the tap geometry): pts (N, ndim) float64 trajectory (device);
+ * dims/gdims HOST arrays of ndim entries.  Writes, in trajectory order, base (3, N) int32 =
+ * ceil(k g / n - w/2) per axis (leading zero rows for 2-D), frac (3, N) float32 offsets whose
+ * KB support decisions equal the reference's float64 ones, and the locality sort key
+ * key (N) int64 = bin * binsize^ndim + cell within bin; *err (device int) is set to 1 if an
+ * offset could not be aligned.  sr_nufft_plan_permute gathers base/frac by a (stable) sort
+ * order of key and writes orig (N) int32 = order. */
+int sr_nufft_plan_geom(const double* pts, long long nsamples, int ndim, const int* dims, const int* gdims,
+                       int width, int binsize, int* base, float* frac, long long* key, int* err, void* stream);
+int sr_nufft_plan_permute(const int* base_in, const float* frac_in, const long long* order, long long nsamples,
+                          int* base_out, float* frac_out, int* orig, void* stream);
 /* Batched unnormalised FFT along the middle axis of an [outer][n][inner] array, in
  * place: inv = 0 natural -> perm order, inv = 1 perm -> natural. */
 int sr_fft_axis(sr_c64* data, long long outer, int n, long long inner, int inv, void* stream);

@@ -55,6 +55,8 @@ SIGNATURES = {
     "sr_nufft_adjoint": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                          _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_partial_blocks": [_ll],
+    "sr_nufft_plan_geom": [_vp, _ll, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "sr_nufft_plan_permute": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
     "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],
 }

@@ -8,11 +8,14 @@ the unnormalised KB window (linops.py:404-410, 464-492), D^-1/2 scaling and G
 factor of the adjoint (linops.py:500-516).  The host builds the plan in fp64
 (tap bases, offsets, apodisation); the device evaluates the KB weights on the
 fly, so no N x G sparse matrix is ever materialised.  Samples are stored in a
-locality-sorted order; forward/adjoint map back to trajectory order.
+locality-sorted order; forward/adjoint map back to trajectory order.  The plan
+(tap bases, offsets, sort, chunk list) is built on the device by default
+(csrc/nufft_plan.cu); the NumPy construction is kept as plan="host".
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 
 import numpy as np
@@ -20,6 +23,8 @@ import torch
 
 from . import _device as dv
 from . import _lib
+
+C_INT = ctypes.c_int
 
 
 def oversampled_dims(dims, oversamp: float) -> tuple[int, ...]:
@@ -88,14 +93,23 @@ class GriddedKernel:
     BIN_CHUNK = 256  # samples per CTA of the binned gridding kernels (nufft.cu)
 
     def __init__(self, dims, points, oversamp: float = 1.25, width: int = 6, binned: bool = True,
-                 binsize: int | None = None):
+                 binsize: int | None = None, plan: str = "device"):
+        """plan: "device" builds the tap geometry, sort and chunk list on the GPU
+        (csrc/nufft_plan.cu); "host" is the NumPy construction.  Both give identical plans."""
         self.dims = tuple(int(n) for n in dims)
         nd = len(self.dims)
         if nd not in (2, 3):
             raise NotImplementedError("device NUFFT implements 2-D and 3-D grids")
-        pts = np.asarray(points, dtype=np.float64)
+        if isinstance(points, torch.Tensor):
+            pts = points.detach()
+            if pts.dtype != torch.float64:
+                raise ValueError("trajectory must be float64")
+        else:
+            pts = np.asarray(points, dtype=np.float64)
         if pts.ndim != 2 or pts.shape[1] != nd:
             raise ValueError("trajectory dimensionality does not match the grid")
+        if plan not in ("device", "host"):
+            raise ValueError("plan must be 'device' or 'host'")
         self.width = int(width)
         if not 1 <= self.width <= 8:
             raise ValueError("KB width must be in [1, 8]")
@@ -104,23 +118,50 @@ class GriddedKernel:
             if not _lib.lib().sr_fft_size_supported(g):
                 raise ValueError(f"oversampled grid axis {g} has no sm_100a FFT instantiation")
         self.betas = [beatty_beta(n, g, self.width) for n, g in zip(self.dims, self.gdims)]
-        self.n_points = pts.shape[0]
+        self.n_points = int(pts.shape[0])
         self.batch = 1
         self.D = int(np.prod(self.dims))
         self.G = int(np.prod(self.gdims))
         self.nmax = self.n_points
-        # tap bases / offsets per axis in fp64 (linops.py:472-476); the fp32 offsets keep the
-        # reference's fp64 support decisions (see support_safe_frac)
-        w = self.width
+        # bins: tile of binsize^d grid cells holding each sample's first tap; samples sorted by bin
+        # and, inside a bin, by first-tap cell
+        self.binsize = int(binsize or (8 if nd == 3 else 16))
+        self.binned = bool(binned)
+        dev = dv.require_cuda()
+        self.device = dev
+        pad = 3 - nd
+        if plan == "device":
+            self.base, self.frac, self.orig, chunks = self._plan_device(pts)
+        else:
+            self.base, self.frac, self.orig, chunks = self._plan_host(
+                pts.cpu().numpy() if isinstance(pts, torch.Tensor) else pts)
+        self.nchunks = int(chunks.shape[0])
+        self.chunks = chunks
+        self.dims3 = torch.tensor([1] * pad + list(self.dims), dtype=torch.int32)
+        self.gdims3 = torch.tensor([1] * pad + list(self.gdims), dtype=torch.int32)
+        self.betas3 = torch.tensor([0.0] * pad + self.betas, dtype=torch.float32)
+        self._dims3_d = self.dims3.to(dev)
+        self._gdims3_d = self.gdims3.to(dev)
+        self._betas3_d = self.betas3.to(dev)
+        ia = [np.ones(1)] * pad
+        for n, g, beta in zip(self.dims, self.gdims, self.betas):
+            r = np.arange(n, dtype=np.float64) - n // 2
+            ia.append(1.0 / kb_apodization(r / g, self.width, beta))
+        self.ia = [dv.host_to_dev(v.astype(np.float32), torch.float32, dev) for v in ia]
+        self._grids = None
+        self._wcache: dict = {}
+        self.nparts = max(_lib.lib().sr_nufft_partial_blocks(self.n_points), self.nchunks)
+
+    def _plan_host(self, pts: np.ndarray):
+        """NumPy plan: tap bases / offsets per axis in fp64 (linops.py:472-476); the fp32 offsets
+        keep the reference's fp64 support decisions (see support_safe_frac)."""
+        nd, w, B = len(self.dims), self.width, self.binsize
         bases, fracs = [], []
         for a, (n, g) in enumerate(zip(self.dims, self.gdims)):
             u = pts[:, a] * (g / n)
             b = np.ceil(u - w / 2.0)
             bases.append(b.astype(np.int64))
             fracs.append(support_safe_frac(u, b, w))
-        # bins: tile of binsize^d grid cells holding each sample's first tap; samples sorted by bin
-        self.binsize = int(binsize or (8 if nd == 3 else 16))
-        B = self.binsize
         bpos = [np.mod(bases[a], g) for a, g in enumerate(self.gdims)]
         nbins = [-(-g // B) for g in self.gdims]
         binid = np.zeros(self.n_points, dtype=np.int64)
@@ -131,7 +172,6 @@ class GriddedKernel:
         # within a bin, samples sharing a first-tap cell are adjacent: the spread merges such
         # runs in registers before its shared atomics (about 3 samples per cell at config 4)
         order = np.argsort(binid * B ** nd + local, kind="stable")
-        self.order = order
         chunks = []
         if self.n_points:
             sb = binid[order]
@@ -146,34 +186,65 @@ class GriddedKernel:
                 coords = [0] * (3 - nd) + coords[::-1]
                 for c0 in range(st, en, self.BIN_CHUNK):
                     chunks.append(coords + [c0, min(self.BIN_CHUNK, en - c0)])
-        self.binned = bool(binned)
-        self.nchunks = len(chunks)
         pad = 3 - nd
         base3 = np.zeros((3, self.n_points), dtype=np.int32)
         frac3 = np.zeros((3, self.n_points), dtype=np.float32)
         for a in range(nd):
             base3[pad + a] = bases[a][order]
             frac3[pad + a] = fracs[a][order]
-        dev = dv.require_cuda()
-        self.device = dev
-        self.base = dv.host_to_dev(base3, torch.int32, dev)
-        self.frac = dv.host_to_dev(frac3, torch.float32, dev)
-        self.orig = dv.host_to_dev(order.astype(np.int32), torch.int32, dev)
-        self.dims3 = torch.tensor([1] * pad + list(self.dims), dtype=torch.int32)
-        self.gdims3 = torch.tensor([1] * pad + list(self.gdims), dtype=torch.int32)
-        self.betas3 = torch.tensor([0.0] * pad + self.betas, dtype=torch.float32)
-        self._dims3_d = self.dims3.to(dev)
-        self._gdims3_d = self.gdims3.to(dev)
-        self._betas3_d = self.betas3.to(dev)
-        ia = [np.ones(1)] * pad
-        for n, g, beta in zip(self.dims, self.gdims, self.betas):
-            r = np.arange(n, dtype=np.float64) - n // 2
-            ia.append(1.0 / kb_apodization(r / g, self.width, beta))
-        self.ia = [dv.host_to_dev(v.astype(np.float32), torch.float32, dev) for v in ia]
-        self.chunks = dv.host_to_dev(np.asarray(chunks, dtype=np.int32).reshape(-1, 5), torch.int32, dev)
-        self._grids = None
-        self._wcache: dict = {}
-        self.nparts = max(_lib.lib().sr_nufft_partial_blocks(self.n_points), self.nchunks)
+        dev = self.device
+        return (dv.host_to_dev(base3, torch.int32, dev), dv.host_to_dev(frac3, torch.float32, dev),
+                dv.host_to_dev(order.astype(np.int32), torch.int32, dev),
+                dv.host_to_dev(np.asarray(chunks, dtype=np.int32).reshape(-1, 5), torch.int32, dev))
+
+    def _plan_device(self, pts):
+        """Device plan (csrc/nufft_plan.cu): per-sample geometry and sort key in a kernel, a stable
+        device radix sort, a gather by the order, and the chunk list from the bin boundaries."""
+        nd, B, N, dev = len(self.dims), self.binsize, self.n_points, self.device
+        CH = self.BIN_CHUNK
+        if isinstance(pts, torch.Tensor):
+            pts_d = pts.to(dev).contiguous()
+        else:
+            pts_d = torch.from_numpy(np.ascontiguousarray(pts)).pin_memory().to(dev, non_blocking=True)
+        base_u = torch.empty(3, N, dtype=torch.int32, device=dev)
+        frac_u = torch.empty(3, N, dtype=torch.float32, device=dev)
+        key = torch.empty(N, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        dims_h = (C_INT * nd)(*self.dims)
+        gdims_h = (C_INT * nd)(*self.gdims)
+        _lib.call("sr_nufft_plan_geom", dv.ptr(pts_d), N, nd, dims_h, gdims_h, self.width, B, dv.ptr(base_u),
+                  dv.ptr(frac_u), dv.ptr(key), dv.ptr(err), dv.stream())
+        skey, order = torch.sort(key, stable=True)
+        base = torch.empty_like(base_u)
+        frac = torch.empty_like(frac_u)
+        orig = torch.empty(N, dtype=torch.int32, device=dev)
+        _lib.call("sr_nufft_plan_permute", dv.ptr(base_u), dv.ptr(frac_u), dv.ptr(order), N, dv.ptr(base),
+                  dv.ptr(frac), dv.ptr(orig), dv.stream())
+        del base_u, frac_u, key, order
+        if N == 0:
+            chunks = torch.zeros(0, 5, dtype=torch.int32, device=dev)
+        else:
+            binid = skey // (B ** nd)
+            change = torch.ones(N, dtype=torch.bool, device=dev)
+            change[1:] = binid[1:] != binid[:-1]
+            starts = torch.nonzero(change).flatten()
+            ends = torch.cat([starts[1:], torch.tensor([N], device=dev)])
+            nch = (ends - starts + CH - 1) // CH
+            owner = torch.repeat_interleave(torch.arange(len(starts), device=dev), nch)
+            first = torch.cumsum(nch, 0) - nch
+            c0 = starts[owner] + (torch.arange(len(owner), device=dev) - first[owner]) * CH
+            cnt = torch.minimum(torch.full_like(c0, CH), ends[owner] - c0)
+            bid = binid[starts][owner]
+            nbins = [-(-g // B) for g in self.gdims]
+            coords = []
+            for a in range(nd - 1, -1, -1):
+                coords.append((bid % nbins[a]) * B)
+                bid = bid // nbins[a]
+            cols = [torch.zeros_like(c0)] * (3 - nd) + coords[::-1] + [c0, cnt]
+            chunks = torch.stack(cols, dim=1).to(torch.int32).contiguous()
+        if int(err.item()):
+            raise RuntimeError("could not align float32 KB support decisions with float64")
+        return base, frac, orig, chunks
 
     # ------------------------------------------------------------ helpers
     def workspace(self, ncoils: int, batch: int | None = None, chunk: int = 0, normal: bool = True):

@@ -533,3 +533,40 @@ def test_graphed_inner_loop_matches_eager(cuda):
         res.append(eng.run(4, 5))
     assert torch.equal(res[0].x, res[1].x)
     np.testing.assert_array_equal(np.asarray(res[0].objectives), np.asarray(res[1].objectives))
+
+
+def _plan_cases():
+    from paper_2305_06482_b200 import synth
+    cases = []
+    for name in ("nufft_2x_w4", "nufft_125_w4", "nufft_125_w6", "nufft3d"):
+        g = golden(name)
+        cases.append((name, tuple(g["dims"]), g["points"], float(g["oversamp"]), int(g["width"])))
+    # equatorial cone samples lie on grid lines up to 1e-16 (support-edge nudging)
+    cases.append(("cones", (40, 48, 24), synth.cones_3d((40, 48, 24), n_readouts=200, n_samples=160), 1.25, 4))
+    cases.append(("radial", (64, 80), synth.golden_angle_radial(40, 128, (64, 80)), 2.0, 4))
+    cases.append(("grid_lines", (32, 32), np.round(np.random.default_rng(2).uniform(-16, 16, (4000, 2)) * 2) / 2
+                  * (2 * np.pi / 32), 2.0, 4))
+    return cases
+
+
+def test_device_plan_equals_host_plan(cuda):
+    """The device plan (csrc/nufft_plan.cu: fp64 tap geometry, support-edge alignment, sort key,
+    gather, chunk list) is bit-identical to the NumPy plan, and both give the same operator."""
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    for name, dims, pts, os_, w in _plan_cases():
+        for bs in (None, 4):
+            kd = GriddedKernel(dims, pts, os_, w, binsize=bs, plan="device")
+            kh = GriddedKernel(dims, pts, os_, w, binsize=bs, plan="host")
+            for f in ("base", "frac", "orig", "chunks"):
+                a, b = getattr(kd, f), getattr(kh, f)
+                assert a.shape == b.shape and a.dtype == b.dtype, (name, f)
+                assert torch.equal(a, b), (name, bs, f)
+            assert kd.nchunks == kh.nchunks
+
+
+def test_device_plan_empty_trajectory(cuda):
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    k = GriddedKernel((16, 16), np.zeros((0, 2)), 2.0, 4, plan="device")
+    assert k.n_points == 0 and k.nchunks == 0
+    with pytest.raises(ValueError):
+        GriddedKernel((16, 16), np.zeros((5, 2)), 2.0, 4, plan="gpu")
