@@ -3,10 +3,12 @@
 
 Emits ``dft_gen.cuh``: one ``__device__ __forceinline__`` function per
 (size, direction) that transforms ``float2 v[N]`` in place, natural order in
-and natural order out.  Composite sizes are unrolled four-step (Cooley-Tukey)
-factorizations whose inner twiddles are literal constants computed here in
-float64 and rounded once to float32, so no sin/cos is evaluated on the device
-for the in-register stages.
+and natural order out.  Sizes with two coprime factors use the prime-factor
+(Good-Thomas) algorithm -- the index maps are free register renaming, and there
+are no inter-stage twiddles (20 = 4 x 5: 272 -> ~224 FP instructions); prime
+powers are unrolled four-step (Cooley-Tukey) factorizations whose inner
+twiddles are literal constants computed here in float64 and rounded once to
+float32, so no sin/cos is evaluated on the device for the in-register stages.
 
 Convention (matches numpy.fft, which the reference uses at
 /root/reference/pkg/src/sketchrecon/linops.py:304-309):
@@ -137,6 +139,18 @@ class _Emitter:
             iq1 = self.muli(q1, sign)
             iq2 = self.muli(q2, sign)
             return [y0, self.add(r1, iq1), self.add(r2, iq2), self.sub(r2, iq2), self.sub(r1, iq1)]
+        a, b = _coprime_split(n)
+        if a > 1:
+            # prime-factor (Good-Thomas) algorithm, gcd(a, b) = 1: input x[(b n1 + a n2) mod n],
+            # output X[(k1 b (b^-1 mod a) + k2 a (a^-1 mod b)) mod n]; no twiddle multiplications
+            inner = [self.dft([xs[(b * n1 + a * n2) % n] for n2 in range(b)], sign) for n1 in range(a)]
+            ea, eb = b * pow(b, -1, a), a * pow(a, -1, b)
+            out = [None] * n
+            for k2 in range(b):
+                col = self.dft([inner[n1][k2] for n1 in range(a)], sign)
+                for k1 in range(a):
+                    out[(k1 * ea + k2 * eb) % n] = col[k1]
+            return out
         # composite: n = a * b, x[a_i + a*b_i]
         a = _pick_factor(n)
         b = n // a
@@ -155,6 +169,23 @@ class _Emitter:
             for ka in range(a):
                 out[kb + b * ka] = col[ka]
         return out
+
+
+def _coprime_split(n: int) -> tuple[int, int]:
+    """n = a * b with gcd(a, b) = 1 and a a prime power (the largest one), or (1, n)."""
+    pp, m, f = [], n, 2
+    while m > 1:
+        if m % f == 0:
+            q = 1
+            while m % f == 0:
+                m //= f
+                q *= f
+            pp.append(q)
+        f += 1
+    if len(pp) < 2:
+        return 1, n
+    a = max(pp)
+    return a, n // a
 
 
 def _pick_factor(n: int) -> int:
