@@ -74,6 +74,13 @@ int sr_group_ngroups(int ny, int nx);
 /* Tuning: prefer group size g where an instantiation exists (0 = each size's default). */
 int sr_group_select(int g);
 
+/* chunk == -3 (split-column schedule, cart_split.cu; square images of the instantiated sizes):
+ * three launches whose middle pass is register-only -- the column FFT's DFT_Q step runs in the
+ * row passes, which own the rows it combines.  sr_split_tune sets the middle pass's coils per
+ * CTA (jc, default 4) and the number of coil ranges the first pass splits a slice into (ja,
+ * default 2). */
+int sr_split_tune(int jc, int ja);
+
 /* Tuning of the three-launch schedule: coils per CTA of the column pass (0 = one coil per
  * CTA, the generic kernel; default 4). */
 int sr_cart_tune(int col_jc);
