@@ -123,6 +123,8 @@ class CartesianKernel:
         lane i % lanes (own stream and workspace), so two small-grid K1 launches share the GPU.
 
         x_host/out_host: pinned (B, D) complex64 CPU tensors.  Returns out_host (synchronised).
+        `chunks` = number of equal chunks, or a sequence of slice counts summing to B (a small
+        last chunk shortens the pipeline drain: its K1 + D2H are all that follow the last H2D).
         `buffers` = (x_dev, out_dev) device staging tensors to reuse across calls.
         """
         import torch
@@ -130,9 +132,16 @@ class CartesianKernel:
             raise ValueError("normal_host takes host tensors")
         ncoils, _ = self._maps_stride(maps)
         B = self.batch
-        chunks = max(1, min(int(chunks), B))
-        lanes = max(1, min(int(lanes), chunks))
-        bounds = [(B * i // chunks, B * (i + 1) // chunks) for i in range(chunks)]
+        if isinstance(chunks, (list, tuple)):
+            sizes = [int(c) for c in chunks]
+            if sum(sizes) != B or min(sizes) < 1:
+                raise ValueError("chunk sizes must be positive and sum to the batch")
+            edges = np.cumsum([0] + sizes)
+            bounds = [(int(edges[i]), int(edges[i + 1])) for i in range(len(sizes))]
+        else:
+            nch = max(1, min(int(chunks), B))
+            bounds = [(B * i // nch, B * (i + 1) // nch) for i in range(nch)]
+        lanes = max(1, min(int(lanes), len(bounds)))
         if buffers is None:
             buffers = (torch.empty(B, self.D, dtype=torch.complex64, device=self.device),
                        torch.empty(B, self.D, dtype=torch.complex64, device=self.device))

@@ -162,20 +162,22 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256):
     # decoupling (K8) is exercised per rank on its own slab (its slices' readout transform):
     kx = torch.fft.fftshift(torch.fft.fft(torch.fft.ifftshift(y2.permute(1, 0, 2), dim=1), dim=1, norm="ortho"), dim=1)
     dec = ReadoutDecoupler(nloc) if _lib_supported(nloc) else None
-    torch.cuda.synchronize()
-    t_start = time.perf_counter()
-    y = dec(kx.contiguous()) if dec is not None else y2
-    torch.cuda.synchronize()
-    t_dec = time.perf_counter()
-    maps0, y0, comp = compress_slices(maps, y, C)
-    torch.cuda.synchronize()
-    t_comp = time.perf_counter()
     reg = so.make_regularizer("l1-wavelet", 1e-3, lo.GridShape(dims))
     cfg = cs.CoilSketchConfig(C, sk.SketchConfig(V + S, V, S, rademacher_scale=12 ** -0.5), reg, 10, 10)
-    t_solve0 = time.perf_counter()
-    res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
-    torch.cuda.synchronize()
-    t_end = time.perf_counter()
+    # the pipeline runs twice; the first run (library handles, graph capture, allocator) is a warm-up
+    for _rep in range(2):
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        y = dec(kx.contiguous()) if dec is not None else y2
+        torch.cuda.synchronize()
+        t_dec = time.perf_counter()
+        maps0, y0, comp = compress_slices(maps, y, C)
+        torch.cuda.synchronize()
+        t_comp = time.perf_counter()
+        t_solve0 = time.perf_counter()
+        res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
+        torch.cuda.synchronize()
+        t_end = time.perf_counter()
     full = gather_slices(res.x, nslices_total, rank, world)
     t_wall = _max_over_ranks(t_end - t_start, world, dev)
     t_solve = _max_over_ranks(t_end - t_solve0, world, dev)
@@ -228,8 +230,11 @@ def run_cfg4(with_oracle: bool, scale: float = 1.0, outer: int = 10, inner: int 
     pts = synth.cones_3d(dims, n_readouts=int(18000 * scale * scale), n_samples=int(512 * scale))
     N = len(pts)
     rng = np.random.default_rng(0)
+    GriddedKernel(dims, pts[:4096], 1.25, 4)  # warm-up (sort / allocator first use)
+    torch.cuda.synchronize()
     t_plan0 = time.perf_counter()
-    kern = GriddedKernel(dims, pts, 1.25, 4)
+    kern = GriddedKernel(dims, pts, 1.25, 4)  # device plan (csrc/nufft_plan.cu), host fp64 trajectory in
+    torch.cuda.synchronize()
     t_plan = time.perf_counter() - t_plan0
     D = kern.D
     maps = synth.coil_maps_cylinder(dims, C, rng, xp=torch, device=dev).unsqueeze(0).contiguous()  # (1, C, D)

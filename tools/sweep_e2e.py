@@ -19,7 +19,10 @@ def main():
     out_host = torch.empty_like(x_host).pin_memory()
     stage = (torch.empty_like(x), torch.empty_like(x))
     for spec in (sys.argv[1] if len(sys.argv) > 1 else "8:1,8:2,16:2,16:3").split(","):
-        ch, lanes = (int(v) for v in spec.split(":"))
+        # "n:lanes" (n equal chunks) or "s1/s2/.../sk:lanes" (explicit slice counts)
+        c, lanes = spec.split(":")
+        ch = [int(v) for v in c.split("/")] if "/" in c else int(c)
+        lanes = int(lanes)
         steps = 20
         t = bench.time_applies(lambda: kern.normal_host(smaps, x_host, out_host, chunks=ch, buffers=stage,
                                                         lanes=lanes), steps, 3, torch.cuda.synchronize)
