@@ -503,25 +503,40 @@ int launch_colpass_t(float2* ws, const uint8_t* maskT, long long mbs, float msca
   return SR_OK;
 }
 
+template <int P, int Q, int NX>
+int launch_colnormal(float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, cudaStream_t st) {
+  using C = ColCfg<P, Q>;
+  const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k_colnormal<P, Q, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return SR_ECUDA;
+    configured = true;
+  }
+  const int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
+  dim3 grid(NX / C::CB, (ncoils + jc - 1) / jc, batch);
+  k_colnormal<P, Q, NX><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
+
+// non-square grids with a coil-looped column pass: (column length ny = P Q, row length nx)
+// -- config 2's 256 x 160 readout-decoupled slices
+#define SR_COLNORMAL_RECT(X) X(16, 16, 160)
+
 template <int P, int Q>
 int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
                    int batch, int ncoils, int nx, cudaStream_t st) {
   using C = ColCfg<P, Q>;
   if constexpr (P > 1 && (P % 4) == 0 && ((P * Q) % C::CB) == 0 && C::CB * Q <= C::T) {
-    if (mode == COL_NORMAL && mscale == 1.f && nx == P * Q && sr_g_col_jc > 0) {
-      const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
-      static bool configured = false;
-      if (!configured) {
-        if (cudaFuncSetAttribute(k_colnormal<P, Q, P * Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-          return SR_ECUDA;
-        configured = true;
-      }
-      const int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
-      dim3 grid(nx / C::CB, (ncoils + jc - 1) / jc, batch);
-      k_colnormal<P, Q, P * Q><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
-      SR_CHECK_LAUNCH();
-      return SR_OK;
+    if (mode == COL_NORMAL && mscale == 1.f && sr_g_col_jc > 0) {
+      if (nx == P * Q) return launch_colnormal<P, Q, P * Q>(ws, maskT, mbs, batch, ncoils, st);
+#define X(P_, Q_, NX_)                                                                    \
+      if constexpr (P == P_ && Q == Q_)                                                   \
+        if (nx == NX_) return launch_colnormal<P_, Q_, NX_>(ws, maskT, mbs, batch, ncoils, st);
+      SR_COLNORMAL_RECT(X)
+#undef X
     }
   }
   if (nx == P * Q && P > 1)
