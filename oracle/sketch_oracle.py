@@ -495,6 +495,69 @@ def pdhg_tv(normal_s, dvec: np.ndarray, anchor: np.ndarray, dims, lam: float, it
     return x
 
 
+def pdhg_reconstruct_tv(a: "Sense", y: np.ndarray, dims, lam: float, iters: int, cg_iters: int,
+                        ratio: float = 1.0, step_scale: float = 0.9, tol: float = 0.0) -> tuple[np.ndarray, int]:
+    """Full-operator l1-TV reconstruction, reconstruct(..., solver="pdhg") (solvers.py:470-500):
+    Chambolle-Pock with K = D (solvers.py:315-362), f* prox = clamp to |p| <= lam, and the data
+    prox argmin_u 0.5||Au - y||^2 + ||u - v||^2/(2 tau) = v + w, w from cg_iters CG steps on
+    (A^H A + I/tau) w = A^H (y - A v) started at 0.  Returns (x, iterations run)."""
+    norm_k = 2.0 * math.sqrt(len(dims))
+    r = math.sqrt(ratio)
+    sigma = r / norm_k * step_scale
+    tau = 1.0 / (r * norm_k) * step_scale
+    x = np.zeros(int(np.prod(dims)), dtype=np.complex128)
+    z = x.copy()
+    p = np.zeros(len(dims) * x.size, dtype=np.complex128)
+    it = 0
+    for it in range(1, iters + 1):
+        p = clamp_magnitude(p + sigma * finite_diff_forward(z, dims), lam)
+        v = x - tau * finite_diff_adjoint(p, dims)
+        rhs = a.adjoint(y - a.forward(v))
+        w = cg(lambda u: a.adjoint(a.forward(u)) + u / tau, rhs, np.zeros_like(v), cg_iters)
+        x_new = v + w
+        z = 2.0 * x_new - x
+        delta = float(np.linalg.norm(x_new - x))
+        xnorm = float(np.linalg.norm(x))
+        x = x_new
+        if xnorm > 0 and delta / xnorm < tol:
+            break
+    return x, it
+
+
+def accproxsgd(a: "Sense", y: np.ndarray, prox, batch: int, alpha0: float, beta: float, beta_min: float,
+               x0: np.ndarray, iters: int, seed: int = 0, tol: float = 0.0) -> tuple[np.ndarray, int]:
+    """Accelerated proximal SGD over coil batches (solvers.py:369-427): per iteration `batch`
+    coils drawn without replacement from seed_stream(seed, 0) (sorted), gradient
+    (C/batch) A_S^H (A_S z - y_S), step max(beta^t alpha0, beta_min), prox, Nesterov momentum.
+    The coil subset shares the kernel and counter (forward_model.py:198-203)."""
+    C = a.n_coils
+    if not 1 <= batch <= C:
+        raise ValueError(f"batch must be in [1, {C}], got {batch}")
+    rng = seed_stream(seed, 0)
+    y_mat = np.asarray(y, dtype=np.complex128).reshape(C, -1)
+    scale = C / batch
+    x = np.array(x0, dtype=np.complex128)
+    z = x.copy()
+    t = 1.0
+    it = 0
+    for it in range(1, iters + 1):
+        idx = np.sort(rng.choice(C, size=batch, replace=False))
+        w = None if a.sqrt_w is None else a.sqrt_w ** 2
+        sub = Sense(a.maps[idx], a.kernel, w, a.counter)
+        g = scale * sub.adjoint(sub.forward(z) - y_mat[idx].ravel())
+        alpha = max(beta ** it * alpha0, beta_min)
+        xn = prox(z - alpha * g, alpha)
+        tn = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t * t))
+        z = xn + ((t - 1.0) / tn) * (xn - x)
+        delta = float(np.linalg.norm(xn - x))
+        xnorm = float(np.linalg.norm(x))
+        x = xn
+        t = tn
+        if xnorm > 0 and delta / xnorm < tol:
+            break
+    return x, it
+
+
 def power_start_vector(dim: int, seed: int = 0) -> np.ndarray:
     g = seed_stream(seed, 0)
     v = g.standard_normal(dim) + 1j * g.standard_normal(dim)

@@ -1,12 +1,11 @@
 """Iterative solvers and proximal maps (mirrors solvers.py of the reference).
 
 Same signatures and semantics as /root/reference/pkg/src/sketchrecon/solvers.py
-for the pairings on the sketched-operator path (l2 -> CG, l1-wavelet ->
-FISTA).  Callbacks receive and return complex64 CUDA tensors; vector algebra
-runs in the device kernels of csrc/vecops.cu, norms/dots are fixed-order
-device reductions.  The l1-TV / PDHG / AccProxSGD pairings are outside the
-hot-path scope and raise
-NotImplementedError.
+for the three regularizer pairings (l2 -> CG, l1-wavelet -> FISTA, l1-tv -> PDHG
+with the inner-CG data prox) and the AccProxSGD baseline over coil batches.
+Callbacks receive and return complex64 CUDA tensors; vector algebra runs in the
+device kernels of csrc/vecops.cu and csrc/tv.cu, norms/dots are fixed-order
+device reductions.
 """
 
 from __future__ import annotations
@@ -337,13 +336,177 @@ def reconstruct(a: SenseOperator, y, reg: Regularizer, cfg: SolverConfig, x0: Im
         return fista(grad, prox, lipschitz, x0, cfg,
                      objective=lambda v: composite_objective(a, y, reg, v), op_for_count=a)
     if solver == "pdhg":
-        raise NotImplementedError("PDHG (l1-tv) is outside the sketched-operator hot-path scope")
+        if reg.kind != "l1-tv":
+            raise ValueError("pdhg is paired with the l1-tv regularizer")
+        return _pdhg_tv(a, y, reg, x0, cfg)
     raise ValueError(f"unknown solver {solver!r}")
 
 
-def pdhg(*args, **kwargs):
-    raise NotImplementedError("PDHG is outside the sketched-operator hot-path scope (SURVEY.md 2, row 9b)")
+def _pdhg_steps(norm_K: float, cfg: SolverConfig) -> tuple[float, float]:
+    ratio = math.sqrt(cfg.pdhg_sigma_tau_ratio)
+    sigma = ratio / norm_K * cfg.step_scale
+    tau = 1.0 / (ratio * norm_K) * cfg.step_scale
+    if sigma * tau * norm_K ** 2 > 1.0 + 1e-12:
+        raise ValueError("step-size product violates sigma*tau*||K||^2 <= 1")
+    return sigma, tau
 
 
-def accproxsgd(*args, **kwargs):
-    raise NotImplementedError("AccProxSGD is outside the sketched-operator hot-path scope (SURVEY.md 2, row 9b)")
+def pdhg(K: LinOp, prox_fdual, prox_g, x0: Image, cfg: SolverConfig, norm_K: float | None = None,
+         objective=None, op_for_count: LinOp | None = None) -> SolveResult:
+    """Chambolle-Pock primal-dual iteration for min_x g(x) + f(K x) (solvers.py:315-362).
+
+    K acts on device tensors; prox_fdual(p, sigma) / prox_g(v, tau) receive and return complex64
+    CUDA tensors.  The axpys run in the sr_lincomb kernel, norms in the fixed-order reductions."""
+    t0 = time.perf_counter()
+    n0 = _coil_count(op_for_count) if op_for_count is not None else 0
+    if norm_K is None:
+        norm_K = math.sqrt(max(normal_max_eig(K, iters=30, seed=0), 1e-30))
+    sigma, tau = _pdhg_steps(norm_K, cfg)
+    x = dv.c64(x0.values).reshape(-1).clone()
+    z = x.clone()
+    p = torch.zeros(K.out_dim, dtype=torch.complex64, device=x.device)
+    hist = []
+    iters = 0
+    for iters in range(1, cfg.max_iters + 1):
+        kz = K.forward(z)
+        lincomb(kz, p, kz, cx=1.0, cy=sigma)
+        p = prox_fdual(kz, sigma)
+        ka = K.adjoint(p)
+        lincomb(ka, x, ka, cx=1.0, cy=-tau)
+        x_new = prox_g(ka, tau)
+        z = torch.empty_like(x_new)
+        lincomb(z, x_new, x, cx=2.0, cy=-1.0)
+        done = False
+        if cfg.tol > 0:
+            diff = torch.empty_like(x_new)
+            lincomb(diff, x_new, x, cx=1.0, cy=-1.0)
+            delta = math.sqrt(float(dev_norm2(diff.view(1, -1))[0]))
+            x_norm = math.sqrt(float(dev_norm2(x.view(1, -1))[0]))
+            done = x_norm > 0 and delta / x_norm < cfg.tol
+        x = x_new
+        if cfg.record_history and objective is not None:
+            hist.append(objective(x))
+        if done:
+            break
+    return SolveResult(Image(x0.shape, x), iters, np.array(hist),
+                       (_coil_count(op_for_count) - n0) if op_for_count is not None else 0,
+                       time.perf_counter() - t0)
+
+
+def clamp_magnitude(p: torch.Tensor, radius: float, shape: GridShape) -> torch.Tensor:
+    """Project each complex entry of a (ndim * D) dual variable onto |p| <= radius
+    (_clamp_magnitude, solvers.py:138-142), in place, by the dual-step kernel with sigma = 0."""
+    import ctypes
+    dims = (ctypes.c_int * shape.ndim)(*shape.dims)
+    zero_img = torch.zeros(shape.size, dtype=torch.complex64, device=p.device)
+    sig0 = torch.zeros(1, dtype=torch.float32, device=p.device)
+    _lib.call("sr_tv_dual", dv.ptr(p), dv.ptr(zero_img), dims, shape.ndim, 0, dv.ptr(sig0), float(radius), 1,
+              dv.stream())
+    return p
+
+
+def _pdhg_tv(a: SenseOperator, y, reg: Regularizer, x0: Image, cfg: SolverConfig) -> SolveResult:
+    """reconstruct(l1-tv) -> PDHG with K = D, f* prox = clamp to lam, and the data prox
+    v + argmin_w from inner CG on (A^H A + I/tau) w = A^H (y - A v) (solvers.py:470-500).
+    The dual step p = clamp(p + sigma D z, lam) and the primal step v = x - tau D^H p are
+    single fused kernels (csrc/tv.cu); the CG matvec is the fused normal operator."""
+    import ctypes
+    shape = reg.transform.shape
+    nd, D = shape.ndim, shape.size
+    dims = (ctypes.c_int * nd)(*shape.dims)
+    sigma, tau = _pdhg_steps(tv_op_norm(nd), cfg)
+    t0 = time.perf_counter()
+    n0 = _coil_count(a)
+    yt = dv.c64(y).reshape(-1)
+    x = dv.c64(x0.values).reshape(1, D).clone()
+    z = x.clone()
+    v = torch.empty_like(x)
+    p = torch.zeros(1, nd * D, dtype=torch.complex64, device=x.device)
+    sig_t = torch.full((1,), sigma, dtype=torch.float32, device=x.device)
+    tau_t = torch.full((1,), tau, dtype=torch.float32, device=x.device)
+    nop = _NormalOp(a)
+    st = dv.stream()
+
+    def matvec(u):
+        out = nop._forward(u)
+        lincomb(out, out, u, cx=1.0, cy=1.0 / tau)
+        return out
+
+    hist = []
+    iters = 0
+    for iters in range(1, cfg.max_iters + 1):
+        _lib.call("sr_tv_dual", dv.ptr(p), dv.ptr(z), dims, nd, 0, dv.ptr(sig_t), float(reg.lam), 1, st)
+        _lib.call("sr_tv_primal", dv.ptr(v), dv.ptr(x), dv.ptr(p), dims, nd, dv.ptr(tau_t), 1, st)
+        r = a._forward(v.reshape(-1))
+        lincomb(r, yt, r, cx=1.0, cy=-1.0)
+        rhs = a._adjoint(r)
+        w, _, _ = _cg_loop(matvec, rhs, torch.zeros_like(rhs), cfg.inner_cg_iters, 0.0)
+        x_new = torch.empty_like(x)
+        lincomb(x_new, v, w.view(1, -1), cx=1.0, cy=1.0)
+        lincomb(z, x_new, x, cx=2.0, cy=-1.0)
+        done = False
+        if cfg.tol > 0:
+            diff = torch.empty_like(x)
+            lincomb(diff, x_new, x, cx=1.0, cy=-1.0)
+            delta = math.sqrt(float(dev_norm2(diff)[0]))
+            x_norm = math.sqrt(float(dev_norm2(x)[0]))
+            done = x_norm > 0 and delta / x_norm < cfg.tol
+        x = x_new
+        if cfg.record_history:
+            hist.append(composite_objective(a, yt, reg, x.reshape(-1)))
+        if done:
+            break
+    return SolveResult(Image(x0.shape, x.reshape(-1)), iters, np.array(hist), _coil_count(a) - n0,
+                       time.perf_counter() - t0)
+
+
+def accproxsgd(op: SenseOperator, y, reg: Regularizer, batch: int, alpha0: float, beta: float,
+               beta_min: float, x0: Image, cfg: SolverConfig, seed: int = 0, objective=None) -> SolveResult:
+    """Accelerated proximal SGD over random coil batches (solvers.py:369-427).
+
+    The coil draws are the reference's (seed_stream(seed, 0).choice, sorted) on the host; each
+    iteration's sub-operator (coil_subset, sharing kernel and counter) runs one forward and one
+    adjoint on the device (2 * batch coil transforms), the prox and momentum are device kernels."""
+    from .rng import seed_stream
+    n_coils = op.n_coils
+    if not 1 <= batch <= n_coils:
+        raise ValueError(f"batch must be in [1, {n_coils}], got {batch}")
+    t0 = time.perf_counter()
+    n0 = _coil_count(op)
+    rng = seed_stream(seed, 0)
+    y_mat = dv.c64(y).reshape(n_coils, op.n_points)
+    scale = n_coils / batch
+    x = dv.c64(x0.values).reshape(-1).clone()
+    z = x.clone()
+    t_k = 1.0
+    hist = []
+    iters = 0
+    for iters in range(1, cfg.max_iters + 1):
+        idx = np.sort(rng.choice(n_coils, size=batch, replace=False))
+        sub = op.coil_subset(idx)
+        ysub = y_mat.index_select(0, torch.as_tensor(idx, device=y_mat.device)).reshape(-1)
+        resid = sub._forward(z)
+        lincomb(resid, resid, ysub, cx=1.0, cy=-1.0)
+        g = sub._adjoint(resid)
+        alpha = max(beta ** iters * alpha0, beta_min)
+        v = torch.empty_like(z)
+        lincomb(v, z, g, cx=1.0, cy=-alpha * scale)
+        x_new = reg.prox(v, alpha)
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_k * t_k))
+        z = torch.empty_like(x_new)
+        lincomb(z, x_new, x, cx=1.0 + (t_k - 1.0) / t_next, cy=-(t_k - 1.0) / t_next)
+        done = False
+        if cfg.tol > 0:
+            diff = torch.empty_like(x_new)
+            lincomb(diff, x_new, x, cx=1.0, cy=-1.0)
+            delta = math.sqrt(float(dev_norm2(diff.view(1, -1))[0]))
+            x_norm = math.sqrt(float(dev_norm2(x.view(1, -1))[0]))
+            done = x_norm > 0 and delta / x_norm < cfg.tol
+        x = x_new
+        t_k = t_next
+        if cfg.record_history and objective is not None:
+            hist.append(objective(x))
+        if done:
+            break
+    return SolveResult(Image(x0.shape, x), iters, np.array(hist), _coil_count(op) - n0,
+                       time.perf_counter() - t0)

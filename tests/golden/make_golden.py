@@ -285,6 +285,38 @@ def main():
                          clamp=so._clamp_magnitude(yy, 0.8),
                          value=np.array(so.make_regularizer("l1-tv", 0.3, tv_shape).value(xx)))
 
+    # --- full-coil solver baselines (appended last): reconstruct(l1-tv -> pdhg) and accproxsgd
+    #     (solvers.py:315-362, 369-427, 434-500)
+    dims = (24, 20)
+    shape = lo.GridShape(dims)
+    maps = smooth_maps(g, dims, 6)
+    pts = random_mask_points(g, dims, 0.35)
+    traj = lo.Trajectory(pts, "cartesian-mask")
+    a = fm.build_sense(fm.SensitivityMaps(shape, maps), traj)
+    grids = np.meshgrid(*[np.linspace(-1, 1, n, endpoint=False) for n in dims], indexing="ij")
+    img = np.zeros(dims, complex)
+    for _ in range(3):
+        c = g.uniform(-0.4, 0.4, 2); ax = g.uniform(0.15, 0.5, 2)
+        img += g.uniform(0.2, 1.0) * (sum(((gg - cc) / aa) ** 2 for gg, cc, aa in zip(grids, c, ax)) <= 1)
+    clean = a.forward(img.ravel())
+    y = clean + (g.standard_normal(clean.shape) + 1j * g.standard_normal(clean.shape)) * 0.01 * np.abs(clean).max()
+    n0 = a.counts["coil_transform"]
+    cfg_tv = so.SolverConfig(max_iters=6, tol=0.0, inner_cg_iters=4)
+    res = so.reconstruct(a, y, so.make_regularizer("l1-tv", 2e-3, shape), cfg_tv)
+    out["solve_pdhg_tv"] = dict(dims=np.array(dims), points=pts, maps=maps, y=y, lam=np.array(2e-3),
+                                iters=np.array(6), cg_iters=np.array(4), x=res.x.values,
+                                iterations=np.array(res.iterations_run),
+                                counts=np.array(res.coil_transform_count))
+    L = so.normal_max_eig(a)
+    reg_w = so.make_regularizer("l1-wavelet", 1e-3, shape)
+    x0 = lo.Image(shape, np.zeros(shape.size, dtype=np.complex128))
+    res2 = so.accproxsgd(a, y, reg_w, 2, 1.0 / L, 0.95, 0.25 / L, x0, so.SolverConfig(max_iters=8, tol=0.0), seed=3)
+    out["solve_accproxsgd"] = dict(dims=np.array(dims), points=pts, maps=maps, y=y, lam=np.array(1e-3),
+                                   batch=np.array(2), alpha0=np.array(1.0 / L), beta=np.array(0.95),
+                                   beta_min=np.array(0.25 / L), iters=np.array(8), seed=np.array(3),
+                                   x=res2.x.values, iterations=np.array(res2.iterations_run),
+                                   counts=np.array(res2.coil_transform_count), unused_n0=np.array(n0))
+
     only = set(sys.argv[1:])
     written = []
     for k, v in out.items():

@@ -124,3 +124,31 @@ def test_tv_operators():
     assert rel(O.finite_diff_adjoint(g["y"], dims), g["adj"]) < 1e-13
     assert rel(O.clamp_magnitude(g["y"], 0.8), g["clamp"]) < 1e-14
     assert abs(O.tv_norm_value(g["x"], dims, 0.3) - float(g["value"])) < 1e-12 * float(g["value"])
+
+
+def _solver_case(name):
+    g = golden(name)
+    dims = tuple(int(v) for v in g["dims"])
+    a = O.Sense(g["maps"], O.CartesianKernel(dims, g["points"]))
+    return g, dims, a
+
+
+def test_full_operator_pdhg_tv():
+    """reconstruct(l1-tv) -> PDHG with the inner-CG data prox (solvers.py:315-362, 470-500)."""
+    g, dims, a = _solver_case("solve_pdhg_tv")
+    x, it = O.pdhg_reconstruct_tv(a, g["y"], dims, float(g["lam"]), int(g["iters"]), int(g["cg_iters"]))
+    assert it == int(g["iterations"])
+    assert rel(x, g["x"]) < TOL
+    assert a.counter.counts["coil_transform"] == int(g["counts"])
+
+
+def test_accproxsgd():
+    """Accelerated proximal SGD over coil batches (solvers.py:369-427)."""
+    g, dims, a = _solver_case("solve_accproxsgd")
+    lam = float(g["lam"])
+    x, it = O.accproxsgd(a, g["y"], lambda v, s: O.wavelet_prox(v, dims, s, lam), int(g["batch"]),
+                         float(g["alpha0"]), float(g["beta"]), float(g["beta_min"]),
+                         np.zeros(int(np.prod(dims)), complex), int(g["iters"]), seed=int(g["seed"]))
+    assert it == int(g["iterations"])
+    assert rel(x, g["x"]) < TOL
+    assert a.counter.counts["coil_transform"] == int(g["counts"])
