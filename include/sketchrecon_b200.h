@@ -84,6 +84,9 @@ int sr_split_tune(int jc, int ja);
 /* Tuning of the three-launch schedule: coils per CTA of the column pass (0 = one coil per
  * CTA, the generic kernel; default 4). */
 int sr_cart_tune(int col_jc);
+/* Tuning: the coil-looped column pass prefetches the next coil's strip in registers (pf = 1,
+ * 2 CTAs/SM, default) or not (pf = 0, 3 CTAs/SM). */
+int sr_cart_tune_colpf(int pf);
 /* Tuning: the row FFT pass stores its output with TMA bulk copies (bulk = 1), through a
  * coalesced copy-out pass (0), or picks per size (2, default: bulk for 20-element groups with
  * Q >= 12, where it measured faster); rows shorter than min_n always use the copy-out. */

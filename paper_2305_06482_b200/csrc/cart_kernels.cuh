@@ -5,6 +5,7 @@
 #include "fft2step.cuh"
 
 extern int sr_g_col_jc;  // coils per CTA of k_colnormal (0 = use k_colpass); cart.cu
+extern int sr_g_col_pf;  // k_colnormal: 1 = next coil's strip prefetched in registers (2 CTAs/SM), 0 = not (3 CTAs/SM)
 extern int sr_g_row_bulk, sr_g_row_bulk_min_n;  // rowfwd TMA bulk stores (on, min row length); cart.cu
 
 enum { COL_NORMAL = 0, COL_FWD = 1, COL_INV = 2 };
@@ -364,8 +365,8 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
 // CTA's (column, k2) groups are loaded once, and coil j+1's column strip is loaded into
 // registers while coil j is transformed (the load latency is hidden behind steps 2/3).
 // Requires CB * Q <= T (one step-2 group per thread) and full column blocks.
-template <int P, int Q, int NXC>
-__global__ void __launch_bounds__(ColCfg<P, Q>::T, 2)
+template <int P, int Q, int NXC, bool PF>
+__global__ void __launch_bounds__(ColCfg<P, Q>::T, PF ? 2 : 3)
 k_colnormal(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long mask_bstride,
             int ncoils, int jc) {
   using S = FftShape<P, Q>;
@@ -395,19 +396,26 @@ k_colnormal(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long lon
     for (int w4 = 0; w4 < P / 4; ++w4) mw[w4] = s2 ? __ldg(mk + w4) : 0u;
   }
   float2* img0 = ws + ((long long)b * ncoils) * D + (long long)p * NX + c0 + c;
-  float2 rn[Q];
+  float2 rn[PF ? Q : 1];
+  if constexpr (PF) {
 #pragma unroll
-  for (int q = 0; q < Q; ++q) rn[q] = img0[j0 * D + (long long)(P * q) * NX];
+    for (int q = 0; q < Q; ++q) rn[q] = img0[j0 * D + (long long)(P * q) * NX];
+  }
   __syncthreads();
   for (int j = j0; j < j1; ++j) {
     float2* img = img0 + j * D;
     float2 r[Q];
+    if constexpr (PF) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) r[q] = rn[q];
+      for (int q = 0; q < Q; ++q) r[q] = rn[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) r[q] = img[(long long)(P * q) * NX];
+    }
     fft_s1_fwd<P, Q>(r, p, t1);
 #pragma unroll
     for (int kk = 0; kk < Q; ++kk) buf[c * VSP + S::GS * kk + p] = r[kk];
-    if (j + 1 < j1) {
+    if (PF && j + 1 < j1) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) rn[q] = img[D + (long long)(P * q) * NX];
     }
@@ -503,22 +511,28 @@ int launch_colpass_t(float2* ws, const uint8_t* maskT, long long mbs, float msca
   return SR_OK;
 }
 
-template <int P, int Q, int NX>
-int launch_colnormal(float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, cudaStream_t st) {
+template <int P, int Q, int NX, bool PF>
+int launch_colnormal_t(float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, cudaStream_t st) {
   using C = ColCfg<P, Q>;
   const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(k_colnormal<P, Q, NX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(k_colnormal<P, Q, NX, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return SR_ECUDA;
     configured = true;
   }
   const int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
   dim3 grid(NX / C::CB, (ncoils + jc - 1) / jc, batch);
-  k_colnormal<P, Q, NX><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
+  k_colnormal<P, Q, NX, PF><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
   SR_CHECK_LAUNCH();
   return SR_OK;
+}
+
+template <int P, int Q, int NX>
+int launch_colnormal(float2* ws, const uint8_t* maskT, long long mbs, int batch, int ncoils, cudaStream_t st) {
+  if (sr_g_col_pf) return launch_colnormal_t<P, Q, NX, true>(ws, maskT, mbs, batch, ncoils, st);
+  return launch_colnormal_t<P, Q, NX, false>(ws, maskT, mbs, batch, ncoils, st);
 }
 
 // non-square grids with a coil-looped column pass: (column length ny = P Q, row length nx)
