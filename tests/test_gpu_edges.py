@@ -121,3 +121,28 @@ def test_row_pass_store_modes_agree(cuda, dims):
     finally:
         _lib.call("sr_cart_tune_rows", 2, 0)
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dims", [(320, 320), (256, 160), (256, 256)])
+def test_column_pass_prefetch_modes_agree(cuda, dims):
+    """The coil-looped column pass with and without the register prefetch of the next coil's
+    strip (sr_cart_tune_colpf) computes identical results (same arithmetic, different schedule)."""
+    from paper_2305_06482_b200 import _lib
+    rng = np.random.default_rng(12)
+    D = dims[0] * dims[1]
+    half = np.array([n // 2 for n in dims])
+    kern = _kern(dims, [np.argwhere(rng.random(dims) < 0.2) - half for _ in range(2)])
+    maps = _c64((rng.standard_normal((2, 6, D)) + 1j * rng.standard_normal((2, 6, D))) / 2)
+    x = _c64(rng.standard_normal((2, D)) + 1j * rng.standard_normal((2, D)))
+    outs = []
+    try:
+        for pf in (1, 0):
+            _lib.call("sr_cart_tune_colpf", pf)
+            o = torch.empty_like(x)
+            kern.normal(maps, x, o)
+            outs.append(o.cpu().numpy())
+    finally:
+        _lib.call("sr_cart_tune_colpf", 1)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    with pytest.raises(ValueError):
+        _lib.call("sr_cart_tune_colpf", 2)
