@@ -108,6 +108,18 @@ def run_2d(cfgid: int, with_oracle: bool):
         torch.cuda.synchronize()
         runs.append(time.perf_counter() - t0)
     t_gpu = float(np.median(runs))
+    if os.environ.get("SR_PROFILE_RECON"):
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+            cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps), cfg,
+                                    weights=weights, kernel=kern, compress=compress)
+            torch.cuda.synchronize()
+        evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+        busy = sum(e.time_range.end - e.time_range.start for e in evs)
+        span = max(e.time_range.end for e in evs) - min(e.time_range.start for e in evs)
+        print(f"GPU kernels+copies: {len(evs)} events, busy {busy / 1e3:.1f} ms of a {span / 1e3:.1f} ms span",
+              flush=True)
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=14), flush=True)
     line = {"config": cfgid, "what": f"coil-sketched recon {dims} C={C} -> {v}+{s}, {T}x{K} FISTA, {wdesc}",
             "gpu_wall_s": t_gpu, "gpu_wall_s_runs": runs, "compress": compress, "counts": rep.counts.get("coil_transform"),
             "expected_counts": cs.expected_coil_transforms(cfg, so.SolverConfig(tol=0.0)),
