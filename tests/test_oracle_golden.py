@@ -152,3 +152,13 @@ def test_accproxsgd():
     assert it == int(g["iterations"])
     assert rel(x, g["x"]) < TOL
     assert a.counter.counts["coil_transform"] == int(g["counts"])
+
+
+def test_chunked_gridded_kernel_equals_gridded_kernel():
+    """The bounded-memory oracle kernel (per-chunk tap tables, used to time the CPU path at
+    config-4 size) computes exactly what the whole-table oracle does (pinned to the fixtures)."""
+    g = golden("nufft3d")
+    dims = tuple(int(v) for v in g["dims"])
+    k = O.ChunkedGriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]), chunk=7)
+    assert rel(k.apply(g["batch"]), g["fwd"]) < TOL
+    assert rel(k.apply_adjoint(g["y"]), g["adj"]) < TOL
