@@ -138,7 +138,16 @@ def run_2d(cfgid: int, with_oracle: bool):
 
 
 # ----------------------------------------------------------------------------- config 2
-def run_cfg2(with_oracle: bool, nslices_total: int = 256):
+def _oracle_slice(args):
+    """One config-2 slice reconstruction through the oracle (process-pool worker)."""
+    from oracle import sketch_oracle as O
+    yh, mh, dims, pts, C, V, S = args
+    okern = O.CartesianKernel(dims, pts)
+    return O.coil_sketching_recon(yh, mh, dims, lambda: okern, c_hat0=C, v=V, s=S, lam=1e-3, outer=10, inner=10,
+                                  rademacher_scale=12 ** -0.5).x_final
+
+
+def run_cfg2(with_oracle: bool, nslices_total: int = 256, pool: int = 0):
     import torch
     from oracle import sketch_oracle as O
     from paper_2305_06482_b200 import coil_sketch as cs
@@ -217,6 +226,28 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256):
         line["nrmse_vs_oracle_max"] = max(errs)
         line["cpu_oracle_s_per_slice"] = tt / len(errs)
         line["cpu_oracle_extrapolated_s"] = tt / len(errs) * nslices_total
+        if pool > 0:
+            import multiprocessing as mp
+            from concurrent.futures import ProcessPoolExecutor
+            cores = len(os.sched_getaffinity(0))
+            k = min(pool, nloc)
+            tasks = [(yh[sl], mh[sl], dims, pts, C, V, S) for sl in range(k)]
+            # single-threaded BLAS in the spawned workers (read when they import numpy)
+            saved = {v: os.environ.get(v) for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")}
+            for v in saved:
+                os.environ[v] = "1"
+            t0 = time.perf_counter()
+            with ProcessPoolExecutor(max_workers=min(cores, k), mp_context=mp.get_context("spawn")) as ex:
+                outs = list(ex.map(_oracle_slice, tasks))
+            t_pool = time.perf_counter() - t0
+            for v, val in saved.items():
+                if val is None:
+                    os.environ.pop(v, None)
+                else:
+                    os.environ[v] = val
+            line["cpu_pool"] = {"slices": k, "processes": min(cores, k), "cores": cores, "wall_s": t_pool,
+                                "extrapolated_s": t_pool * nslices_total / k,
+                                "nrmse_max": max(_nrmse(xs[sl], outs[sl]) for sl in range(k))}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return full
@@ -349,13 +380,16 @@ def main():
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--slices", type=int, default=256)
     ap.add_argument("--scale", type=float, default=1.0, help="config 4 geometry scale (1.0 = full size)")
+    ap.add_argument("--oracle-pool", type=int, default=0,
+                    help="config 2: also run this many slice reconstructions of the oracle in a process pool "
+                         "(one per host core, OPENBLAS_NUM_THREADS=1) and extrapolate to all slices")
     ap.add_argument("--outer", type=int, default=10)
     ap.add_argument("--inner", type=int, default=10)
     a = ap.parse_args()
     if a.config in (0, 3):
         run_2d(a.config, a.oracle)
     elif a.config == 2:
-        run_cfg2(a.oracle, a.slices)
+        run_cfg2(a.oracle, a.slices, a.oracle_pool)
     else:
         run_cfg4(a.oracle, a.scale, a.outer, a.inner)
 
