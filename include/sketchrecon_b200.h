@@ -134,6 +134,10 @@ int sr_cart_adjoint(const sr_c64* y, long long ystride, const sr_c64* maps,
 int sr_coil_contract(const sr_c64* in, sr_c64* out, const sr_c64* S, long long s_bstride,
                      int batch, int cout, int cin, long long D, long long in_bstride,
                      long long out_bstride, void* stream);
+/* K5, real coefficients (the sketch matrix of sketching.py:69-94): S (batch or 1, cout, cin)
+ * float32, cout <= 32, D even, in/out 16-byte aligned; two voxels per thread. */
+int sr_coil_contract_real(const sr_c64* in, sr_c64* out, const float* S, long long s_bstride, int batch, int cout,
+                          int cin, long long D, long long in_bstride, long long out_bstride, void* stream);
 
 /* K6 -- one level of the 2-D periodic DB4 analysis (linops.py:619-635, 677-687)
  * on the top-left h x w corner (row stride ld, slice stride bs); optional fused

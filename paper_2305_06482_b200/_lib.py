@@ -26,6 +26,7 @@ SIGNATURES = {
     "sr_cart_adjoint": [_vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
                         _vp, _vp, _vp, _vp],
     "sr_coil_contract": [_vp, _vp, _vp, _ll, _i, _i, _i, _ll, _ll, _ll, _vp],
+    "sr_coil_contract_real": [_vp, _vp, _vp, _ll, _i, _i, _i, _ll, _ll, _ll, _vp],
     "sr_wavelet_ana2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _f, _i, _vp, _vp],
     "sr_wavelet_ana2_nblocks": [_i, _i],
     "sr_wavelet_syn2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _vp, _f, _vp],

@@ -146,3 +146,19 @@ def test_column_pass_prefetch_modes_agree(cuda, dims):
     np.testing.assert_array_equal(outs[0], outs[1])
     with pytest.raises(ValueError):
         _lib.call("sr_cart_tune_colpf", 2)
+
+
+@pytest.mark.parametrize("B,C,chat,D", [(3, 32, 12, 4096), (1, 16, 8, 1000), (2, 9, 5, 64), (1, 40, 32, 128)])
+def test_real_sketch_contraction_matches_complex_path(cuda, B, C, chat, D):
+    """K5 with a real coefficient matrix (2 FMAs per MAC, two voxels per thread) equals the
+    general complex-coefficient kernel bit for bit (same fused multiply-adds, zero imaginary part)."""
+    from paper_2305_06482_b200.sketching import coil_contract
+    rng = np.random.default_rng(B * 100 + C)
+    maps = _c64(rng.standard_normal((B, C, D)) + 1j * rng.standard_normal((B, C, D)))
+    S = rng.standard_normal((chat, C))
+    S[:2] = 0
+    S[0, 0] = S[1, 1] = 1.0  # identity rows copy exactly
+    got = coil_contract(maps, S)
+    ref = coil_contract(maps, S.astype(np.complex128))
+    np.testing.assert_array_equal(got.cpu().numpy(), ref.cpu().numpy())
+    np.testing.assert_array_equal(got[:, :2].cpu().numpy(), maps[:, :2].cpu().numpy())

@@ -199,6 +199,12 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256, pool: int = 0):
         res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
         torch.cuda.synchronize()
         t_end = time.perf_counter()
+    if os.environ.get("SR_PROFILE_RECON") and rank == 0:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
+            torch.cuda.synchronize()
+        print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=16), flush=True)
     full = gather_slices(res.x, nslices_total, rank, world)
     t_wall = _max_over_ranks(t_end - t_start, world, dev)
     t_solve = _max_over_ranks(t_end - t_solve0, world, dev)
