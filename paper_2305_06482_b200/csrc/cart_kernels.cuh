@@ -555,6 +555,12 @@ int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale
   }
   if (nx == P * Q && P > 1)
     return launch_colpass_t<P, Q, P * Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+  // compile-time row length for the listed non-square grids too (immediate address offsets)
+#define X(P_, Q_, NX_)                                                                                 \
+  if constexpr (P == P_ && Q == Q_)                                                                    \
+    if (nx == NX_) return launch_colpass_t<P_, Q_, NX_>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+  SR_COLNORMAL_RECT(X)
+#undef X
   return launch_colpass_t<P, Q, 0>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
 }
 
