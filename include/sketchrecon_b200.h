@@ -110,22 +110,31 @@ int sr_fused_stats(unsigned long long* dev_buf);
  *            samples [soff[b], soff[b+1]); y is (batch, ncoils, ystride)
  *   ymeas: NULL, or measured data -> y = A x - ymeas and, if partial != NULL,
  *          partial[(b*ncoils + j)*partial_blocks + k] = sum |y|^2 pieces
- *          (the residual of composite_objective, solvers.py:188-195). */
+ *          (the residual of composite_objective, solvers.py:188-195).
+ *   bptr/bidx/nblk: optional per-column-block sample lists (bptr (batch, nblk+1) absolute
+ *          offsets into bidx = sample indices within the slice grouped by perm-order x block of
+ *          sr_cart_col_block(ny) columns); given, the gather runs inside the column pass
+ *          (nblk partial blocks, the rest zeroed); NULL = separate gather launch. */
 int sr_cart_forward(const sr_c64* x, const sr_c64* maps, long long map_bstride,
                     const int* spos, const sr_c64* ph, const long long* soff,
                     sr_c64* y, long long ystride, const sr_c64* ymeas, double* partial,
                     int partial_blocks, sr_c64* ws, int batch, int ncoils, int ny, int nx,
-                    void* stream);
+                    const int* bptr, const int* bidx, int nblk, void* stream);
+/* Column-block width (x positions per CTA) of the column pass for a column length ny. */
+int sr_cart_col_block(int ny);
 
 /* K2 -- SENSE adjoint A^H y: scatter (last duplicate wins, as numpy fancy
  * assignment at linops.py:357), centered unitary IFFT, conjugate coil sum
  * (forward_model.py:174-180).  wlist/woff: per-slice list of sample indices to
- * write (duplicates removed by the host).  coef/u/d: epilogue as sr_cart_normal. */
+ * write (duplicates removed by the host).  coef/u/d: epilogue as sr_cart_normal.
+ * bptr/bidx/nblk: optional per-column-block lists of the wlist samples (as in sr_cart_forward);
+ * given, the scatter runs inside the column pass (no workspace memset / scatter launch). */
 int sr_cart_adjoint(const sr_c64* y, long long ystride, const sr_c64* maps,
                     long long map_bstride, const int* spos, const sr_c64* ph,
                     const long long* soff, const int* wlist, const long long* woff,
                     sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
-                    const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+                    const float* coef, const sr_c64* u, const sr_c64* d,
+                    const int* bptr, const int* bidx, int nblk, void* stream);
 
 /* K5 -- coil contraction out[b,i,:] = sum_k S[b,i,k] in[b,k,:]:
  * `sketch_maps` (sketching.py:97-103, S real Chat x C) and the map/data rotation

@@ -22,9 +22,11 @@ SIGNATURES = {
     "sr_fft_size_supported": [_i],
     "sr_fft_split": [_i, C.POINTER(_i), C.POINTER(_i)],
     "sr_cart_normal": [_vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _i, _vp],
-    "sr_cart_forward": [_vp, _vp, _ll, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _i, _vp, _i, _i, _i, _i, _vp],
+    "sr_cart_forward": [_vp, _vp, _ll, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _i, _vp, _i, _i, _i, _i,
+                        _vp, _vp, _i, _vp],
+    "sr_cart_col_block": [_i],
     "sr_cart_adjoint": [_vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
-                        _vp, _vp, _vp, _vp],
+                        _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "sr_coil_contract": [_vp, _vp, _vp, _ll, _i, _i, _i, _ll, _ll, _ll, _vp],
     "sr_coil_contract_real": [_vp, _vp, _vp, _ll, _i, _i, _i, _ll, _ll, _ll, _vp],
     "sr_wavelet_ana2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _f, _i, _vp, _vp],

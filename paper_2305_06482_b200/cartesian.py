@@ -58,6 +58,28 @@ class CartesianKernel:
         woff = np.zeros(self.batch + 1, dtype=np.int64)
         woff[1:] = np.cumsum([len(p.wlist) for p in per_slice])
         self.woff = dv.host_to_dev(woff, torch.int64, dev)
+        # per-column-block sample lists: K2 gathers / scatters inside the column pass
+        cb = int(_lib.lib().sr_cart_col_block(self.ny))
+        self.nblk = (self.nx + cb - 1) // cb if cb > 0 else 0
+        self.fused_io = cb > 0
+        if self.fused_io:
+            g_idx, g_ptr, s_idx, s_ptr = [], [], [], []
+            g_base = s_base = 0
+            for p in per_slice:
+                blk = (p.spos.astype(np.int64) % self.nx) // cb
+                order = np.argsort(blk, kind="stable").astype(np.int32)
+                g_idx.append(order)
+                g_ptr.append(g_base + np.r_[0, np.cumsum(np.bincount(blk, minlength=self.nblk))])
+                g_base += len(order)
+                wb = blk[p.wlist]
+                worder = p.wlist[np.argsort(wb, kind="stable")].astype(np.int32)
+                s_idx.append(worder)
+                s_ptr.append(s_base + np.r_[0, np.cumsum(np.bincount(wb, minlength=self.nblk))])
+                s_base += len(worder)
+            self.g_idx = dv.host_to_dev(np.concatenate(g_idx), torch.int32, dev)
+            self.g_ptr = dv.host_to_dev(np.stack(g_ptr), torch.int32, dev)
+            self.s_idx = dv.host_to_dev(np.concatenate(s_idx), torch.int32, dev)
+            self.s_ptr = dv.host_to_dev(np.stack(s_ptr), torch.int32, dev)
         self._ws = None
         self.chunk = 0  # sr_cart_normal schedule: 0 three launches, >0 chunked, -1 persistent fused
         self._plans = plans
@@ -192,10 +214,12 @@ class CartesianKernel:
         if y is None:
             y = torch.zeros(self.batch, ncoils, self.nmax, dtype=torch.complex64, device=self.device)
         ws = self.workspace(ncoils)
+        fused = self.fused_io
         _lib.call("sr_cart_forward", dv.ptr(x), dv.ptr(maps), mbs, dv.ptr(self.spos),
                   dv.ptr(self.ph), dv.ptr(self.soff), dv.ptr(y), y.shape[-1], dv.ptr(ymeas),
                   dv.ptr(partial), partial_blocks, dv.ptr(ws), self.batch, ncoils, self.ny,
-                  self.nx, dv.stream())
+                  self.nx, dv.ptr(self.g_ptr) if fused else None, dv.ptr(self.g_idx) if fused else None,
+                  self.nblk, dv.stream())
         return y
 
     def adjoint(self, maps, y, out, *, coef=None, u=None, d=None, w=None):
@@ -209,7 +233,8 @@ class CartesianKernel:
         _lib.call("sr_cart_adjoint", dv.ptr(y), y.shape[-1], dv.ptr(maps), mbs, dv.ptr(self.spos),
                   dv.ptr(self.ph), dv.ptr(self.soff), dv.ptr(self.wlist), dv.ptr(self.woff),
                   dv.ptr(out), dv.ptr(ws), self.batch, ncoils, self.ny, self.nx, dv.ptr(coef),
-                  dv.ptr(u), dv.ptr(d), dv.stream())
+                  dv.ptr(u), dv.ptr(d), dv.ptr(self.s_ptr) if self.fused_io else None,
+                  dv.ptr(self.s_idx) if self.fused_io else None, self.nblk, dv.stream())
         return out
 
     # ------------------------------------------------- reference plugin protocol

@@ -35,12 +35,22 @@ int SR_CAT(sr_dispatch_rowinv_b, SR_BUCKET_ID)(int nx, const float2* ws, const f
 
 int SR_CAT(sr_dispatch_colpass_b, SR_BUCKET_ID)(int ny, float2* ws, const uint8_t* maskT, long long mbs,
                                                 float mscale, int mode, int batch, int ncoils, int nx,
-                                                cudaStream_t st) {
+                                                cudaStream_t st, const SampleIO* sio) {
   switch (ny) {
 #define X(N, P, Q) \
-  case N: return launch_colpass<P, Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+  case N: return launch_colpass<P, Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st, sio);
     SR_BUCKET_SIZES(X)
 #undef X
     default: return SR_EUNSUPPORTED;
+  }
+}
+
+int SR_CAT(sr_dispatch_colblock_b, SR_BUCKET_ID)(int ny) {
+  switch (ny) {
+#define X(N, P, Q) \
+  case N: return ColCfg<P, Q>::CB;
+    SR_BUCKET_SIZES(X)
+#undef X
+    default: return 0;
   }
 }

@@ -8,12 +8,31 @@ extern int sr_g_col_jc;  // coils per CTA of k_colnormal (0 = use k_colpass); ca
 extern int sr_g_col_pf;  // k_colnormal: 1 = next coil's strip prefetched in registers (2 CTAs/SM), 0 = not (3 CTAs/SM)
 extern int sr_g_row_bulk, sr_g_row_bulk_min_n;  // rowfwd TMA bulk stores (on, min row length); cart.cu
 
-enum { COL_NORMAL = 0, COL_FWD = 1, COL_INV = 2 };
+enum { COL_NORMAL = 0, COL_FWD = 1, COL_INV = 2, COL_FWD_G = 3, COL_INV_S = 4 };
+
+// K2 sample I/O fused into the column pass (modes COL_FWD_G / COL_INV_S): the samples of slice b
+// whose perm-order x position falls in column block k are bidx[bptr[b][k] .. bptr[b][k+1]) (indices
+// within the slice; spos / ph / y as in k_gather / k_scatter).
+struct SampleIO {
+  const int* spos;
+  const float2* ph;
+  const long long* soff;
+  const int* bptr;  // (batch, nblk + 1), absolute offsets into bidx
+  const int* bidx;
+  float2* y;          // COL_FWD_G output
+  const float2* yin;  // COL_INV_S input
+  const float2* ymeas;
+  double* partial;
+  long long ystride;
+  float scale;
+  int nblk, pblocks;
+};
 
 namespace {
 
 // ------------------------------------------------------------------- pass A
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
+__host__ __device__ constexpr int pow2_floor(int n) { return n < 2 ? 1 : 2 * pow2_floor(n / 2); }
 
 // ROWS rows per CTA, one thread per (row, p): T = ROWS * P is a whole number
 // of warps and at least 128 threads.
@@ -266,7 +285,7 @@ struct ColCfg {
 template <int P, int Q, int NXC>
 __global__ void __launch_bounds__(ColCfg<P, Q>::T)
 k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long mask_bstride,
-          float mscale, int mode, int nx_rt, int ncoils) {
+          float mscale, int mode, int nx_rt, int ncoils, SampleIO sio) {
   using S = FftShape<P, Q>;
   constexpr int N = S::N, CB = ColCfg<P, Q>::CB, T = ColCfg<P, Q>::T, VSP = ColCfg<P, Q>::VSP;
   constexpr bool FULL = NXC > 0 && (NXC % CB) == 0;  // every column block is complete
@@ -286,12 +305,28 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
   __syncthreads();
   const int c = tid % CB, p = tid / CB;
   const bool cvalid = FULL || c < ncols;
+  const bool inv_only = (mode == COL_INV || mode == COL_INV_S);
+  const bool fwd_only = (mode == COL_FWD || mode == COL_FWD_G);
 
   if (mode == COL_INV) {
     // spectrum in perm order along y -> smem
     for (int e = tid; e < CB * N; e += T) {
       const int cc = e % CB, pos = e / CB;
       if (cc < ncols) buf[cc * VSP + S::pad(pos)] = img[(long long)pos * nx + c0 + cc];
+    }
+    __syncthreads();
+  } else if (mode == COL_INV_S) {
+    // adjoint sample scatter straight into the zeroed strip (no workspace memset / scatter pass)
+    for (int e = tid; e < CB * VSP; e += T) buf[e] = make_float2(0.f, 0.f);
+    __syncthreads();
+    const long long s0 = sio.soff[b];
+    const int* bp = sio.bptr + (long long)b * (sio.nblk + 1) + blockIdx.x;
+    const long long yo = ((long long)b * ncoils + j) * sio.ystride;
+    for (int t = bp[0] + tid; t < bp[1]; t += T) {
+      const int i = sio.bidx[t];
+      const int sp = sio.spos[s0 + i];
+      const int py = sp / nx, cx = sp - py * nx - c0;
+      buf[cx * VSP + S::pad(py)] = cscale(cmulc(sio.ph[s0 + i], sio.yin[yo + i]), sio.scale);
     }
     __syncthreads();
   } else {
@@ -315,7 +350,7 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
     float2* gp = buf + cc * VSP + S::GS * k2;
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
-    if (mode != COL_INV) fft_s2_fwd<P>(g);
+    if (!inv_only) fft_s2_fwd<P>(g);
     if (mode == COL_NORMAL) {
       const uint8_t* mk = mcol + (long long)(c0 + cc) * N + P * k2;
       if ((P % 4) == 0) {
@@ -337,7 +372,7 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
         for (int k1 = 0; k1 < P; ++k1) g[k1] = cscale(g[k1], mk[k1] ? mscale : 0.f);
       }
     }
-    if (mode != COL_FWD) fft_s2_inv<P, Q>(g, k2, t2);
+    if (!fwd_only) fft_s2_inv<P, Q>(g, k2, t2);
 #pragma unroll
     for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
   }
@@ -347,6 +382,40 @@ k_colpass(float2* __restrict__ ws, const uint8_t* __restrict__ maskT, long long 
     for (int e = tid; e < CB * N; e += T) {
       const int cc = e % CB, pos = e / CB;
       if (cc < ncols) img[(long long)pos * nx + c0 + cc] = buf[cc * VSP + S::pad(pos)];
+    }
+    return;
+  }
+  if (mode == COL_FWD_G) {
+    // forward sample gather straight from the strip (no workspace write / gather pass);
+    // residual y - ymeas and its squared norm per block (deterministic tree reduction)
+    const long long s0 = sio.soff[b];
+    const int* bp = sio.bptr + (long long)b * (sio.nblk + 1) + blockIdx.x;
+    const long long yo = ((long long)b * ncoils + j) * sio.ystride;
+    double acc = 0.0;
+    for (int t = bp[0] + tid; t < bp[1]; t += T) {
+      const int i = sio.bidx[t];
+      const int sp = sio.spos[s0 + i];
+      const int py = sp / nx, cx = sp - py * nx - c0;
+      float2 v = cscale(cmul(sio.ph[s0 + i], buf[cx * VSP + S::pad(py)]), sio.scale);
+      if (sio.ymeas) {
+        v = csub(v, sio.ymeas[yo + i]);
+        acc += (double)v.x * v.x + (double)v.y * v.y;
+      }
+      sio.y[yo + i] = v;
+    }
+    if (sio.partial) {
+      __syncthreads();  // strip no longer read: reuse it for the reduction
+      double* red = reinterpret_cast<double*>(buf);
+      constexpr int T2 = pow2_floor(T);  // fold the tail above the largest power of two first
+      red[tid] = acc;
+      __syncthreads();
+      if (tid >= T2) red[tid - T2] += red[tid];
+      __syncthreads();
+      for (int st = T2 / 2; st > 0; st >>= 1) {
+        if (tid < st) red[tid] += red[tid + st];
+        __syncthreads();
+      }
+      if (tid == 0) sio.partial[((long long)b * ncoils + j) * sio.pblocks + blockIdx.x] = red[0];
     }
     return;
   }
@@ -495,7 +564,7 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
 
 template <int P, int Q, int NXC>
 int launch_colpass_t(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
-                     int batch, int ncoils, int nx, cudaStream_t st) {
+                     int batch, int ncoils, int nx, cudaStream_t st, const SampleIO* sio) {
   using C = ColCfg<P, Q>;
   const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
   static bool configured = false;
@@ -506,7 +575,8 @@ int launch_colpass_t(float2* ws, const uint8_t* maskT, long long mbs, float msca
     configured = true;
   }
   dim3 grid((nx + C::CB - 1) / C::CB, ncoils, batch);
-  k_colpass<P, Q, NXC><<<grid, C::T, smem, st>>>(ws, maskT, mbs, mscale, mode, nx, ncoils);
+  k_colpass<P, Q, NXC><<<grid, C::T, smem, st>>>(ws, maskT, mbs, mscale, mode, nx, ncoils,
+                                                 sio ? *sio : SampleIO{});
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -541,7 +611,7 @@ int launch_colnormal(float2* ws, const uint8_t* maskT, long long mbs, int batch,
 
 template <int P, int Q>
 int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale, int mode,
-                   int batch, int ncoils, int nx, cudaStream_t st) {
+                   int batch, int ncoils, int nx, cudaStream_t st, const SampleIO* sio) {
   using C = ColCfg<P, Q>;
   if constexpr (P > 1 && (P % 4) == 0 && ((P * Q) % C::CB) == 0 && C::CB * Q <= C::T) {
     if (mode == COL_NORMAL && mscale == 1.f && sr_g_col_jc > 0) {
@@ -554,14 +624,14 @@ int launch_colpass(float2* ws, const uint8_t* maskT, long long mbs, float mscale
     }
   }
   if (nx == P * Q && P > 1)
-    return launch_colpass_t<P, Q, P * Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+    return launch_colpass_t<P, Q, P * Q>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st, sio);
   // compile-time row length for the listed non-square grids too (immediate address offsets)
 #define X(P_, Q_, NX_)                                                                                 \
   if constexpr (P == P_ && Q == Q_)                                                                    \
-    if (nx == NX_) return launch_colpass_t<P_, Q_, NX_>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+    if (nx == NX_) return launch_colpass_t<P_, Q_, NX_>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st, sio);
   SR_COLNORMAL_RECT(X)
 #undef X
-  return launch_colpass_t<P, Q, 0>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st);
+  return launch_colpass_t<P, Q, 0>(ws, maskT, mbs, mscale, mode, batch, ncoils, nx, st, sio);
 }
 
 }  // namespace
