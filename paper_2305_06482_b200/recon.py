@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -53,7 +54,7 @@ class EngineResult:
 
 
 _POWER_V0: dict = {}
-GRAPH_MIN_REPLAYED = 400
+GRAPH_MIN_REPLAYED = int(os.environ.get("SR_GRAPH_MIN_REPLAYED", "400"))
 
 
 def _power_start(seed: int, d: int, dev) -> torch.Tensor:
