@@ -306,17 +306,32 @@ k_embed_rows(const RowGeom rg) {
   const float2* ar = rg.anchor ? rg.anchor + pixrow : xr;  // never null-based
   const int h2 = rg.n2 >> 1;
   float2 r[Q];
+  {
+    // all loads of the thread issued back to back from clamped (always valid) addresses, then
+    // selected: the rows are short, so the kernel lives on load latency
+    float2 mv[Q], xv[Q];
+    float iv[Q];
+    bool in[Q];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const int k2 = p + P * q;
-    float2 v = make_float2(0.f, 0.f);
-    if (valid && ax_inside(k2, rg.n2, N)) {
-      const int i2 = (k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2;
-      float2 xv = xr[i2];
-      if (rg.anchor) xv = csub(xv, ar[i2]);
-      v = cscale(cmul(mj[i2], xv), s01 * rg.ia2[i2]);
+    for (int q = 0; q < Q; ++q) {
+      const int k2 = p + P * q;
+      in[q] = valid && ax_inside(k2, rg.n2, N);
+      const int i2 = in[q] ? ((k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2) : 0;
+      mv[q] = mj[i2];
+      xv[q] = xr[i2];
+      iv[q] = rg.ia2[i2];
     }
-    r[q] = v;
+    if (rg.anchor) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int k2 = p + P * q;
+        const int i2 = in[q] ? ((k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2) : 0;
+        xv[q] = csub(xv[q], ar[i2]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      r[q] = in[q] ? cscale(cmul(mv[q], xv[q]), s01 * iv[q]) : make_float2(0.f, 0.f);
   }
   __syncthreads();
   fft_s1_fwd<P, Q>(r, p, tw);
