@@ -249,6 +249,25 @@ int sr_nufft_plan_geom(const double* pts, long long nsamples, int ndim, const in
                        int width, int binsize, int* base, float* frac, long long* key, int* err, void* stream);
 int sr_nufft_plan_permute(const int* base_in, const float* frac_in, const long long* order, long long nsamples,
                           int* base_out, float* frac_out, int* orig, void* stream);
+
+/* Opaque NUFFT plan owned by the library (the whole _build_interpolator of linops.py:464-492 plus
+ * the grid / Beatty beta / apodisation of linops.py:434-462, built on the device from a HOST
+ * float64 trajectory (N, ndim); identical to GriddedKernel's plan).  binsize 0 = default.
+ * sr_nufft_plan_info returns its geometry and device arrays (any pointer may be NULL);
+ * sr_nufft_plan_normal applies the (sketched) SENSE normal operator with it, sqrtw = sqrt of the
+ * density weights in trajectory order (device, NULL = 1), grids as sr_nufft_normal. */
+typedef struct sr_nufft_plan sr_nufft_plan;
+int sr_nufft_plan_create(const double* pts, long long nsamples, int ndim, const int* dims, double oversamp,
+                         int width, int binsize, sr_nufft_plan** out, void* stream);
+int sr_nufft_plan_destroy(sr_nufft_plan* plan);
+int sr_nufft_plan_info(const sr_nufft_plan* plan, int* dims, int* gdims, float* betas, long long* nsamples,
+                       long long* nchunks, const int** base, const float** frac, const int** orig,
+                       const int** chunks, const float** ia0, const float** ia1, const float** ia2);
+int sr_nufft_plan_normal(sr_nufft_plan* plan, const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
+                         const float* sqrtw, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
+                         const sr_c64* d, void* stream);
+/* Device-to-device copy on a stream. */
+int sr_memcpy_d2d(void* dst, const void* src, long long bytes, void* stream);
 /* Batched unnormalised FFT along the middle axis of an [outer][n][inner] array, in
  * place: inv = 0 natural -> perm order, inv = 1 perm -> natural. */
 int sr_fft_axis(sr_c64* data, long long outer, int n, long long inner, int inv, void* stream);

@@ -62,6 +62,11 @@ SIGNATURES = {
     "sr_nufft_partial_blocks": [_ll],
     "sr_nufft_plan_geom": [_vp, _ll, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "sr_nufft_plan_permute": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sr_nufft_plan_create": [_vp, _ll, _i, _vp, C.c_double, _i, _i, _vp, _vp],
+    "sr_nufft_plan_destroy": [_vp],
+    "sr_nufft_plan_info": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_nufft_plan_normal": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_memcpy_d2d": [_vp, _vp, _ll, _vp],
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
     "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],
 }

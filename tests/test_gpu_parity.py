@@ -638,3 +638,57 @@ def test_accproxsgd_matches_reference(cuda):
     with pytest.raises(ValueError):
         so.accproxsgd(a, g["y"], so.make_regularizer("l1-wavelet", 1e-3, shape), 0, 1.0, 0.9, 0.1, x0,
                       so.SolverConfig(max_iters=1))
+
+
+def test_opaque_c_plan_equals_python_plan(cuda):
+    """sr_nufft_plan_create (the C-ABI plan a non-Python caller uses: grid, betas, apodisation,
+    tap geometry, CUB radix sort, chunk list -- all in the library) equals GriddedKernel's plan
+    array for array, and sr_nufft_plan_normal equals GriddedKernel.normal bit for bit."""
+    import ctypes
+    from paper_2305_06482_b200 import _device as dv
+    from paper_2305_06482_b200 import _lib, synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    lib = _lib.lib()
+    cases = [((40, 48, 24), synth.cones_3d((40, 48, 24), n_readouts=200, n_samples=160), 1.25, 4),
+             ((64, 80), synth.golden_angle_radial(40, 128, (64, 80)), 2.0, 4)]
+    g = golden("nufft_125_w6")
+    cases.append((tuple(int(v) for v in g["dims"]), g["points"], 1.25, 6))
+    for dims, pts, os_, w in cases:
+        kern = GriddedKernel(dims, pts, os_, w)
+        nd = len(dims)
+        pts64 = np.ascontiguousarray(pts, dtype=np.float64)
+        plan = ctypes.c_void_p()
+        _lib.call("sr_nufft_plan_create", pts64.ctypes.data, len(pts64), nd, (ctypes.c_int * nd)(*dims), os_, w, 0,
+                  ctypes.byref(plan), dv.stream())
+        try:
+            d3, g3, b3 = (ctypes.c_int * 3)(), (ctypes.c_int * 3)(), (ctypes.c_float * 3)()
+            n, nch = ctypes.c_longlong(), ctypes.c_longlong()
+            ptrs = [ctypes.c_void_p() for _ in range(7)]
+            _lib.call("sr_nufft_plan_info", plan, d3, g3, b3, ctypes.byref(n), ctypes.byref(nch),
+                      *[ctypes.byref(p) for p in ptrs])
+            assert list(d3) == kern.dims3.tolist() and list(g3) == kern.gdims3.tolist()
+            assert np.array_equal(np.array(list(b3), dtype=np.float32), kern.betas3.numpy())
+            assert n.value == kern.n_points and nch.value == kern.nchunks
+
+            def fetch(ptr, like):
+                t = torch.empty_like(like)
+                _lib.call("sr_memcpy_d2d", t.data_ptr(), ptr, t.numel() * t.element_size(), dv.stream())
+                return t
+            for ptr, ref in zip(ptrs[:4], (kern.base, kern.frac, kern.orig, kern.chunks)):
+                assert torch.equal(fetch(ptr.value, ref), ref)
+            for ptr, ref in zip(ptrs[4:], kern.ia):
+                assert torch.equal(fetch(ptr.value, ref), ref)
+            rng = np.random.default_rng(7)
+            D = kern.D
+            maps = torch.from_numpy((rng.standard_normal((2, D)) + 1j * rng.standard_normal((2, D))).astype(
+                np.complex64)).cuda().unsqueeze(0)
+            x = torch.from_numpy((rng.standard_normal(D) + 1j * rng.standard_normal(D)).astype(np.complex64)).cuda()
+            x = x.view(1, -1)
+            o1, o2 = torch.empty_like(x), torch.empty_like(x)
+            kern.normal(maps, x, o1)
+            grids = torch.empty(2 * 2 * kern.G, dtype=torch.complex64, device="cuda")
+            _lib.call("sr_nufft_plan_normal", plan, x.data_ptr(), None, maps.data_ptr(), 2, None, o2.data_ptr(),
+                      grids.data_ptr(), None, None, None, dv.stream())
+            assert rel(o2.cpu().numpy(), o1.cpu().numpy()) < 1e-6
+        finally:
+            _lib.call("sr_nufft_plan_destroy", plan)
