@@ -123,6 +123,33 @@ int sr_cart_forward(const sr_c64* x, const sr_c64* maps, long long map_bstride,
 /* Column-block width (x positions per CTA) of the column pass for a column length ny. */
 int sr_cart_col_block(int ny);
 
+/* Opaque Cartesian plan (the tables of _CartesianMaskKernel, linops.py:332-364, in the device's
+ * perm-order layout: sample offsets, centering phases, transposed mask, adjoint write list with
+ * the last duplicate winning as linops.py:357, per-column-block sample lists), built by the library
+ * from a HOST float64 trajectory: pts (total, ndim) centered integer bins of all slices
+ * concatenated, counts = samples per slice (batch entries; one entry with shared = 1 for one mask
+ * used by every slice); ndim 1 or 2, dims = (ny, nx) or (nx).  Identical to CartesianKernel's
+ * tables.  The _normal / _forward / _adjoint entries take the arguments of sr_cart_normal /
+ * sr_cart_forward / sr_cart_adjoint that the plan does not hold; ws: sr_cart_plan_ws_bytes. */
+typedef struct sr_cart_plan sr_cart_plan;
+int sr_cart_plan_create(const double* pts, const long long* counts, int batch, int ndim, const int* dims,
+                        int shared, sr_cart_plan** out, void* stream);
+int sr_cart_plan_destroy(sr_cart_plan* plan);
+int sr_cart_plan_info(const sr_cart_plan* plan, int* ny, int* nx, long long* nmax, long long* total,
+                      long long* wtotal, int* nblk, const int** spos, const sr_c64** ph, const long long** soff,
+                      const int** wlist, const long long** woff, const uint8_t** maskT, const int** g_ptr,
+                      const int** g_idx, const int** s_ptr, const int** s_idx);
+long long sr_cart_plan_ws_bytes(const sr_cart_plan* plan, int ncoils);
+int sr_cart_plan_normal(const sr_cart_plan* plan, const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
+                        long long map_bstride, int ncoils, sr_c64* out, sr_c64* ws, const float* coef,
+                        const sr_c64* u, const sr_c64* d, void* stream);
+int sr_cart_plan_forward(const sr_cart_plan* plan, const sr_c64* x, const sr_c64* maps, long long map_bstride,
+                         int ncoils, sr_c64* y, long long ystride, const sr_c64* ymeas, double* partial,
+                         int partial_blocks, sr_c64* ws, void* stream);
+int sr_cart_plan_adjoint(const sr_cart_plan* plan, const sr_c64* y, long long ystride, const sr_c64* maps,
+                         long long map_bstride, int ncoils, sr_c64* out, sr_c64* ws, const float* coef,
+                         const sr_c64* u, const sr_c64* d, void* stream);
+
 /* K2 -- SENSE adjoint A^H y: scatter (last duplicate wins, as numpy fancy
  * assignment at linops.py:357), centered unitary IFFT, conjugate coil sum
  * (forward_model.py:174-180).  wlist/woff: per-slice list of sample indices to

@@ -25,6 +25,13 @@ SIGNATURES = {
     "sr_cart_forward": [_vp, _vp, _ll, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _i, _vp, _i, _i, _i, _i,
                         _vp, _vp, _i, _vp],
     "sr_cart_col_block": [_i],
+    "sr_cart_plan_create": [_vp, _vp, _i, _i, _vp, _i, _vp, _vp],
+    "sr_cart_plan_destroy": [_vp],
+    "sr_cart_plan_info": [_vp] + [_vp] * 16,
+    "sr_cart_plan_ws_bytes": [_vp, _i],
+    "sr_cart_plan_normal": [_vp, _vp, _vp, _vp, _ll, _i, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_cart_plan_forward": [_vp, _vp, _vp, _ll, _i, _vp, _ll, _vp, _vp, _i, _vp, _vp],
+    "sr_cart_plan_adjoint": [_vp, _vp, _ll, _vp, _ll, _i, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_cart_adjoint": [_vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i,
                         _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "sr_coil_contract": [_vp, _vp, _vp, _ll, _i, _i, _i, _ll, _ll, _ll, _vp],
@@ -70,7 +77,8 @@ SIGNATURES = {
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
     "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],
 }
-RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong}
+RESTYPES = {"sr_host_vd_poisson": C.c_longlong, "sr_cart_ws_bytes": C.c_longlong,
+            "sr_cart_plan_ws_bytes": C.c_longlong}
 
 _ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError}
 _MESSAGES = {1: "invalid argument or shape", 2: "unsupported transform length",

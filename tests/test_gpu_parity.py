@@ -692,3 +692,70 @@ def test_opaque_c_plan_equals_python_plan(cuda):
             assert rel(o2.cpu().numpy(), o1.cpu().numpy()) < 1e-6
         finally:
             _lib.call("sr_nufft_plan_destroy", plan)
+
+
+def test_opaque_cartesian_plan_equals_python_plan(cuda):
+    """sr_cart_plan_create (the library-built Cartesian tables of the C ABI) equals CartesianKernel's
+    tables array for array, and the plan's normal / forward / adjoint equal the kernel methods."""
+    import ctypes
+    from paper_2305_06482_b200 import _device as dv
+    from paper_2305_06482_b200 import _lib
+    from paper_2305_06482_b200.cartesian import CartesianKernel
+    from paper_2305_06482_b200.plan import cartesian_plan
+    rng = np.random.default_rng(31)
+    cases = []
+    for dims, B, shared in (((320, 320), 3, False), ((256, 160), 4, True), ((60,), 2, False), ((64, 40), 1, False)):
+        half = np.array([n // 2 for n in dims])
+        pl = []
+        for b in range(1 if shared else B):
+            pts = np.argwhere(rng.random(dims) < 0.2 + 0.1 * b) - half
+            pts = np.concatenate([pts, pts[: max(1, len(pts) // 9)]]).astype(np.float64)  # duplicates
+            pl.append(pts)
+        cases.append((dims, B, shared, pl))
+    for dims, B, shared, pl in cases:
+        kern = CartesianKernel(dims, [cartesian_plan(dims, p) for p in pl], batch=B)
+        allp = np.ascontiguousarray(np.concatenate(pl), dtype=np.float64)
+        counts = (ctypes.c_longlong * len(pl))(*[len(p) for p in pl])
+        plan = ctypes.c_void_p()
+        _lib.call("sr_cart_plan_create", allp.ctypes.data, counts, B, len(dims), (ctypes.c_int * len(dims))(*dims),
+                  1 if shared else 0, ctypes.byref(plan), dv.stream())
+        try:
+            ny, nx, nblk = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+            nmax, tot, wtot = ctypes.c_longlong(), ctypes.c_longlong(), ctypes.c_longlong()
+            ptrs = [ctypes.c_void_p() for _ in range(10)]
+            _lib.call("sr_cart_plan_info", plan, ctypes.byref(ny), ctypes.byref(nx), ctypes.byref(nmax),
+                      ctypes.byref(tot), ctypes.byref(wtot), ctypes.byref(nblk), *[ctypes.byref(p) for p in ptrs])
+            assert (ny.value, nx.value, nmax.value, nblk.value) == (kern.ny, kern.nx, kern.nmax, kern.nblk)
+
+            def fetch(ptr, like):
+                t = torch.empty_like(like)
+                _lib.call("sr_memcpy_d2d", t.data_ptr(), ptr, t.numel() * t.element_size(), dv.stream())
+                return t
+            refs = (kern.spos, kern.ph, kern.soff, kern.wlist, kern.woff, kern.maskT, kern.g_ptr, kern.g_idx,
+                    kern.s_ptr, kern.s_idx)
+            for name, ptr, ref in zip(("spos", "ph", "soff", "wlist", "woff", "maskT", "g_ptr", "g_idx", "s_ptr",
+                                       "s_idx"), ptrs, refs):
+                assert torch.equal(fetch(ptr.value, ref.contiguous()), ref), (dims, name)
+            C = 3
+            D = kern.D
+            maps = torch.from_numpy(((rng.standard_normal((B, C, D)) + 1j * rng.standard_normal((B, C, D))) / 2)
+                                    .astype(np.complex64)).cuda()
+            x = torch.from_numpy((rng.standard_normal((B, D)) + 1j * rng.standard_normal((B, D))).astype(np.complex64)).cuda()
+            ws = torch.empty((_lib.lib().sr_cart_plan_ws_bytes(plan, C) + 7) // 8, dtype=torch.complex64, device="cuda")
+            o1, o2 = torch.empty_like(x), torch.empty_like(x)
+            kern.normal(maps, x, o1)
+            _lib.call("sr_cart_plan_normal", plan, x.data_ptr(), None, maps.data_ptr(), C * D, C, o2.data_ptr(),
+                      ws.data_ptr(), None, None, None, dv.stream())
+            assert torch.equal(o1, o2)
+            y1 = kern.forward(maps, x)
+            y2 = torch.zeros_like(y1)
+            _lib.call("sr_cart_plan_forward", plan, x.data_ptr(), maps.data_ptr(), C * D, C, y2.data_ptr(),
+                      y2.shape[-1], None, None, 0, ws.data_ptr(), dv.stream())
+            assert torch.equal(y1, y2)
+            a1, a2 = torch.empty_like(x), torch.empty_like(x)
+            kern.adjoint(maps, y1, a1)
+            _lib.call("sr_cart_plan_adjoint", plan, y1.data_ptr(), y1.shape[-1], maps.data_ptr(), C * D, C,
+                      a2.data_ptr(), ws.data_ptr(), None, None, None, dv.stream())
+            assert torch.equal(a1, a2)
+        finally:
+            _lib.call("sr_cart_plan_destroy", plan)
