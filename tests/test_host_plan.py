@@ -111,3 +111,35 @@ def test_support_safe_frac_keeps_float64_decisions():
             ref = (1.0 - (2.0 * (u - (b + k)) / w) ** 2) > 0
             dev = np.abs((np.float32(2.0) * (t - np.float32(k))) / np.float32(w)) < np.float32(1.0)
             assert np.array_equal(ref, dev), (w, k)
+
+
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    out = tmp_path / "c_abi_normal"
+    libdir = ROOT / "paper_2305_06482_b200" / "_native"
+    cmd = [gcc, "-O2", "-std=c11", f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include", "-o", str(out),
+           str(ROOT / "examples" / "c_abi_normal.c"), f"-L{libdir}", "-lsketchrecon_b200",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lm", f"-Wl,-rpath,{libdir}", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_c_abi_example_compiles_and_links(tmp_path):
+    """The header is plain C and the library exports what a C caller links (examples/)."""
+    assert _build_c_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_abi_example_runs(tmp_path):
+    """A pure-C caller (no Python / torch): library-owned Cartesian plan + normal op vs a direct
+    CPU DFT (examples/c_abi_normal.c exits 0 when the relative L2 error is below 1e-4)."""
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
