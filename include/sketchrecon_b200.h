@@ -293,6 +293,10 @@ int sr_nufft_plan_info(const sr_nufft_plan* plan, int* dims, int* gdims, float* 
 int sr_nufft_plan_normal(sr_nufft_plan* plan, const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
                          const float* sqrtw, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
                          const sr_c64* d, void* stream);
+/* Batched tall-skinny Householder QR, R only (LAPACK zgeqr2 / zlarfg conventions), complex128:
+ * A (batch, N, C) row-major blocks Y^H (overwritten), R (batch, C, C); C <= 32.  The LQ step of
+ * numpy's SVD of a wide C x N block (coil_compress_svd, forward_model.py:245-272). */
+int sr_tsqr_r(void* A, long long N, int C, long long a_bstride, int batch, void* R, void* stream);
 /* Device-to-device copy on a stream. */
 int sr_memcpy_d2d(void* dst, const void* src, long long bytes, void* stream);
 /* Batched unnormalised FFT along the middle axis of an [outer][n][inner] array, in

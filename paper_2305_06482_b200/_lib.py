@@ -74,6 +74,7 @@ SIGNATURES = {
     "sr_nufft_plan_info": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_nufft_plan_normal": [_vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_memcpy_d2d": [_vp, _vp, _ll, _vp],
+    "sr_tsqr_r": [_vp, _ll, _i, _ll, _i, _vp, _vp],
     "sr_fft_axis": [_vp, _ll, _i, _ll, _i, _vp],
     "sr_readout_idft": [_vp, _vp, _vp, _vp, _i, _i, _ll, _vp],
 }

@@ -132,8 +132,17 @@ def slice_compression(y: torch.Tensor, keep: int, valid_n=None, threads: int | N
             y[s, :, int(valid_n[s]):] = 0
     if N < C:
         raise ValueError("compression needs at least as many samples as coils")
-    a, _ = torch.geqrf(y.to(torch.complex128).conj().transpose(1, 2).contiguous())
-    R = torch.triu(a[:, :C, :]).cpu().numpy()
+    A = y.to(torch.complex128).conj().transpose(1, 2).contiguous()
+    if C <= 32:
+        # batched tall-skinny Householder kernel (csrc/tsqr.cu), one CTA per slice
+        from . import _device as dv
+        from . import _lib
+        Rt = torch.empty(S, C, C, dtype=torch.complex128, device=y.device)
+        _lib.call("sr_tsqr_r", A.data_ptr(), N, C, N * C, S, Rt.data_ptr(), dv.stream())
+        R = Rt.cpu().numpy()
+    else:
+        a, _ = torch.geqrf(A)
+        R = torch.triu(a[:, :C, :]).cpu().numpy()
 
     def one(s):
         u, _, _ = np.linalg.svd(R[s].conj().T, full_matrices=False)
