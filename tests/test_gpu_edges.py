@@ -197,3 +197,21 @@ def test_fused_sample_io_matches_separate_passes(cuda, dims, C):
         np.testing.assert_allclose(outs[True][0][b, :, :n], outs[False][0][b, :, :n], rtol=0, atol=2e-6)
     assert np.abs(outs[True][1] - outs[False][1]).max() <= 1e-6 * max(1.0, np.abs(outs[False][1]).max())
     np.testing.assert_allclose(outs[True][2], outs[False][2], rtol=1e-7)
+
+
+@pytest.mark.parametrize("S,N,C", [(4, 5119, 32), (3, 700, 12), (2, 40, 40 // 2), (1, 33, 32)])
+def test_tsqr_r_matches_lapack(cuda, S, N, C):
+    """Batched tall-skinny Householder R (csrc/tsqr.cu) equals LAPACK's zgeqrf R (numpy.linalg.qr,
+    mode 'r') including the signs of its real diagonal; a zero column takes the tau = 0 path."""
+    from paper_2305_06482_b200 import _device as dv
+    from paper_2305_06482_b200 import _lib
+    rng = np.random.default_rng(S * N + C)
+    A = (rng.standard_normal((S, N, C)) + 1j * rng.standard_normal((S, N, C))) * np.exp(rng.standard_normal((S, 1, C)))
+    A[0, :, min(3, C - 1)] = 0.0
+    At = torch.from_numpy(A).cuda().contiguous()
+    R = torch.empty(S, C, C, dtype=torch.complex128, device="cuda")
+    _lib.call("sr_tsqr_r", At.data_ptr(), N, C, N * C, S, R.data_ptr(), dv.stream())
+    R = R.cpu().numpy()
+    for s in range(S):
+        ref = np.linalg.qr(A[s], mode="r")
+        np.testing.assert_allclose(R[s], ref, rtol=0, atol=1e-10 * np.abs(ref).max())
