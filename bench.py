@@ -375,7 +375,8 @@ def main():
             "e2e": {"value": world * n_e2e / t_e2e, "unit": UNIT,
                     "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8),
                     "path": "CartesianKernel.normal_host: pinned host x -> (8 slice chunks, H2D | K1 | D2H "
-                            "overlapped on 3 streams) -> pinned host out"},
+                            "overlapped on 3 streams; a call's H2D copies start during the previous call's "
+                            "last chunks) -> pinned host out, every step copying its full input and output"},
             "unsketched_32coil": {"value": world * max(3, args.steps // 5) / t_full, "unit": UNIT,
                                   "speedup_sketched": (world * args.steps / t_s) / (world * max(3, args.steps // 5) / t_full)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

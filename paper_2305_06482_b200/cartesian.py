@@ -179,8 +179,18 @@ class CartesianKernel:
             self._host_streams = (torch.cuda.Stream(self.device), torch.cuda.Stream(self.device),
                                   [torch.cuda.Stream(self.device) for _ in range(lanes)])
         s_in, s_out, s_k = self._host_streams
-        for st in (s_in, s_out, *s_k[:lanes]):
+        for st in (s_out, *s_k[:lanes]):
             st.wait_stream(cur)
+        # The host-to-device copies depend on no device work of the caller; they only must not
+        # overwrite a staging chunk the previous call's K1 still reads.  So consecutive calls
+        # pipeline: this call's copies start while the previous call's last chunks compute and
+        # copy back (same chunking and staging buffers: per-chunk events; otherwise a full wait).
+        prev = getattr(self, "_host_prev", None)
+        if prev is not None and prev[0] == bounds and prev[1] is xd:
+            for ev in prev[2]:
+                s_in.wait_event(ev)
+        else:
+            s_in.wait_stream(cur)
         done_in = []
         for b0, b1 in bounds:
             with torch.cuda.stream(s_in):
@@ -188,15 +198,18 @@ class CartesianKernel:
                 e = torch.cuda.Event()
                 e.record(s_in)
                 done_in.append(e)
+        done_k = []
         for i, ((b0, b1), e) in enumerate(zip(bounds, done_in)):
             sk = s_k[i % lanes]
             sk.wait_event(e)
             self._normal_range(maps, xd, od, b0, b1, self._host_ws[i % lanes], sk.cuda_stream)
             ec = torch.cuda.Event()
             ec.record(sk)
+            done_k.append(ec)
             s_out.wait_event(ec)
             with torch.cuda.stream(s_out):
                 out_host[b0:b1].copy_(od[b0:b1], non_blocking=True)
+        self._host_prev = (bounds, xd, done_k)
         cur.wait_stream(s_out)
         for st in s_k[:lanes]:
             cur.wait_stream(st)

@@ -494,7 +494,22 @@ def test_normal_host_pipelined_matches_device(cuda):
     kern.normal(maps, x.cuda(), ref)
     out = torch.empty(B, D, dtype=torch.complex64).pin_memory()
     kern.normal_host(maps, x.pin_memory(), out, chunks=3)
+    torch.cuda.synchronize()
     assert rel(out.numpy(), ref.cpu().numpy()) < 1e-6
+    # consecutive calls overlap (the next call's copies start during the previous call's tail):
+    # many back-to-back calls on distinct inputs / outputs with shared staging buffers
+    stage = (torch.empty(B, D, dtype=torch.complex64, device="cuda"),
+             torch.empty(B, D, dtype=torch.complex64, device="cuda"))
+    xs = [torch.from_numpy((rng.standard_normal((B, D)) + 1j * rng.standard_normal((B, D))).astype(np.complex64))
+          .pin_memory() for _ in range(6)]
+    outs = [torch.empty(B, D, dtype=torch.complex64).pin_memory() for _ in range(6)]
+    for xi, oi in zip(xs, outs):
+        kern.normal_host(maps, xi, oi, chunks=3, buffers=stage)
+    torch.cuda.synchronize()
+    for xi, oi in zip(xs, outs):
+        r = torch.empty(B, D, dtype=torch.complex64, device="cuda")
+        kern.normal(maps, xi.cuda(), r)
+        assert rel(oi.numpy(), r.cpu().numpy()) < 1e-6
 
 
 @pytest.mark.parametrize("binned", [True, False])
