@@ -24,7 +24,7 @@ INCLUDE = ROOT / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-         "-Xptxas", "-O3", f"-I{INCLUDE}", f"-I{CSRC}"]
+         "-Xptxas", "-O3", f"-I{INCLUDE}", f"-I{CSRC}"] + os.environ.get("SR_NVCC_EXTRA", "").split()
 
 
 def _sources():

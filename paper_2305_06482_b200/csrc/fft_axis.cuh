@@ -3,6 +3,14 @@
 #pragma once
 #include "fft2step.cuh"
 
+// minimum resident CTAs per SM for the fused row passes of the gridded NUFFT (register caps)
+#ifndef SR_EMBED_MINB
+#define SR_EMBED_MINB 1
+#endif
+#ifndef SR_CROP_MINB
+#define SR_CROP_MINB 1
+#endif
+
 // Zero-padding structure of an oversampled NUFFT axis of length g holding an image axis of
 // length n (centered: image index i sits at grid index (i - n/2) mod g, linops.py:438-446).
 static __device__ __forceinline__ bool ax_inside(int k, int n, int g) {
@@ -273,7 +281,7 @@ int launch_strided(float2* data, long long outer, long long inner, int inv, cuda
 }
 
 template <int P, int Q>
-__global__ void __launch_bounds__(AxCfg<P, Q>::T)
+__global__ void __launch_bounds__(AxCfg<P, Q>::T, SR_EMBED_MINB)
 k_embed_rows(const RowGeom rg) {
   using S = FftShape<P, Q>;
   using A = AxCfg<P, Q>;
@@ -359,7 +367,7 @@ k_embed_rows(const RowGeom rg) {
 }
 
 template <int P, int Q>
-__global__ void __launch_bounds__(AxCfg<P, Q>::T)
+__global__ void __launch_bounds__(AxCfg<P, Q>::T, SR_CROP_MINB)
 k_rows_crop(const RowGeom rg) {
   using S = FftShape<P, Q>;
   using A = AxCfg<P, Q>;
