@@ -326,7 +326,7 @@ def main():
     stage = (torch.empty_like(x), torch.empty_like(x))
 
     def e2e_step():
-        kern.normal_host(smaps, x_host, out_host, chunks=8, buffers=stage)
+        kern.normal_host(smaps, x_host, out_host, chunks=8, buffers=stage, overlap_prev=True)
 
     t_e2e = time_applies(e2e_step, max(5, args.steps // 2), 2, barrier_sync)
     n_e2e = max(5, args.steps // 2)

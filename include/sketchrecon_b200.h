@@ -129,7 +129,8 @@ int sr_cart_col_block(int ny);
  * from a HOST float64 trajectory: pts (total, ndim) centered integer bins of all slices
  * concatenated, counts = samples per slice (batch entries; one entry with shared = 1 for one mask
  * used by every slice); ndim 1 or 2, dims = (ny, nx) or (nx).  Identical to CartesianKernel's
- * tables.  The _normal / _forward / _adjoint entries take the arguments of sr_cart_normal /
+ * tables.  Returns SR_EINVAL if any coordinate lies outside [-n/2, n/2) on its axis, as
+ * Trajectory.validate_for (linops.py:130-140) rejects it.  The _normal / _forward / _adjoint entries take the arguments of sr_cart_normal /
  * sr_cart_forward / sr_cart_adjoint that the plan does not hold; ws: sr_cart_plan_ws_bytes. */
 typedef struct sr_cart_plan sr_cart_plan;
 int sr_cart_plan_create(const double* pts, const long long* counts, int batch, int ndim, const int* dims,
@@ -264,13 +265,32 @@ int sr_nufft_adjoint(const sr_c64* y, const sr_c64* maps, int ncoils, const int*
                      long long nsamples, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
                      const sr_c64* d, const int* chunks, int nchunks, int binsize, void* stream);
 int sr_nufft_partial_blocks(long long nsamples);
+/* 3-D Cartesian mask kernel (_CartesianMaskKernel on a 3-D grid, linops.py:332-364, which the
+ * 2-D K1/K2 kernels do not cover): the grid pipeline of the NUFFT entries with g = n and unit
+ * apodisation.  dims (3, HOST ints, axes with sr_fft_size_supported lengths); ones0..2 device
+ * float vectors of ones (lengths dims[a]); spos (N) int32 perm-layout offset of each sample,
+ * sum_a perm(f_a mod n_a) * stride_a; mask (n0 n1 n2) uint8 sampled-bin indicator in the same
+ * layout; wlist (nw) the last occurrence of every distinct bin (linops.py:357); grids ncoils * D
+ * complex64 workspace; y / ymeas (ncoils, ystride); partial: sr_cart3_partial_blocks(N, ncoils)
+ * doubles of |A x - y|^2 when ymeas is given.  Epilogue coef/u/d as sr_cart_normal. */
+int sr_cart3_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils, const int* dims,
+                    const float* ones0, const float* ones1, const float* ones2, const unsigned char* mask,
+                    sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, void* stream);
+int sr_cart3_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int* dims, const float* ones0,
+                     const float* ones1, const float* ones2, const int* spos, long long nsamples, sr_c64* y,
+                     long long ystride, const sr_c64* ymeas, double* partial, sr_c64* grids, void* stream);
+int sr_cart3_adjoint(const sr_c64* y, long long ystride, const sr_c64* maps, int ncoils, const int* dims,
+                     const float* ones0, const float* ones1, const float* ones2, const int* spos,
+                     const int* wlist, long long nw, sr_c64* out, sr_c64* grids, const float* coef, const sr_c64* u,
+                     const sr_c64* d, void* stream);
+int sr_cart3_partial_blocks(long long nsamples, int ncoils);
 /* NUFFT plan on the device (replaces the host loop of _GriddedNUFFTKernel._build_interpolator,
  * linops.py:464-492, for the tap geometry): pts (N, ndim) float64 trajectory (device);
  * dims/gdims HOST arrays of ndim entries.  Writes, in trajectory order, base (3, N) int32 =
  * ceil(k g / n - w/2) per axis (leading zero rows for 2-D), frac (3, N) float32 offsets whose
  * KB support decisions equal the reference's float64 ones, and the locality sort key
  * key (N) int64 = bin * binsize^ndim + cell within bin; *err (device int) is set to 1 if an
- * offset could not be aligned.  sr_nufft_plan_permute gathers base/frac by a (stable) sort
+ * offset could not be aligned or a coordinate lies outside [-n/2, n/2) (linops.py:130-140).  sr_nufft_plan_permute gathers base/frac by a (stable) sort
  * order of key and writes orig (N) int32 = order. */
 int sr_nufft_plan_geom(const double* pts, long long nsamples, int ndim, const int* dims, const int* gdims,
                        int width, int binsize, int* base, float* frac, long long* key, int* err, void* stream);

@@ -625,13 +625,17 @@ def power_start_vector(dim: int, seed: int = 0) -> np.ndarray:
     return v / np.linalg.norm(v)
 
 
-def fista(grad, prox, L: float, x0: np.ndarray, iters: int, tol: float = 0.0) -> np.ndarray:
-    """FISTA, t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2 (solvers.py:264-308)."""
+def fista(grad, prox, L: float, x0: np.ndarray, iters: int, tol: float = 0.0, objective=None,
+          full: bool = False):
+    """FISTA, t_{k+1} = (1 + sqrt(1 + 4 t_k^2))/2 (solvers.py:264-308).  full=True returns
+    (x, iterations run, objective history)."""
     step = 1.0 / L
     x = np.array(x0, dtype=np.complex128)
     z = x.copy()
     t = 1.0
-    for _ in range(iters):
+    hist = []
+    it = 0
+    for it in range(1, iters + 1):
         xn = prox(z - step * grad(z), step)
         tn = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t * t))
         z = xn + ((t - 1.0) / tn) * (xn - x)
@@ -639,19 +643,25 @@ def fista(grad, prox, L: float, x0: np.ndarray, iters: int, tol: float = 0.0) ->
         xnorm = float(np.linalg.norm(x))
         x = xn
         t = tn
+        if objective is not None:
+            hist.append(objective(x))
         if xnorm > 0 and delta / xnorm < tol:
             break
-    return x
+    return (x, it, np.array(hist)) if full else x
 
 
-def cg(matvec, b, x0, iters: int, tol_abs: float = 0.0):
-    """Plain CG on M x = b (solvers.py:206-229)."""
+def cg(matvec, b, x0, iters: int, tol_abs: float = 0.0, full: bool = False):
+    """Plain CG on M x = b (solvers.py:206-229).  full=True returns (x, iterations, residual
+    norms)."""
     x = np.array(x0, dtype=np.complex128)
     r = b - matvec(x) if np.any(x) else np.array(b, dtype=np.complex128)
     p = r.copy()
     rs = float(np.real(np.vdot(r, r)))
-    for _ in range(iters):
+    res = [math.sqrt(rs)]
+    it = 0
+    for it in range(1, iters + 1):
         if math.sqrt(rs) <= tol_abs:
+            it -= 1
             break
         mp = matvec(p)
         den = float(np.real(np.vdot(p, mp)))
@@ -661,9 +671,66 @@ def cg(matvec, b, x0, iters: int, tol_abs: float = 0.0):
         x = x + a * p
         r = r - a * mp
         rn = float(np.real(np.vdot(r, r)))
+        res.append(math.sqrt(rn))
         p = r + (rn / rs) * p
         rs = rn
-    return x
+    return (x, it, np.array(res)) if full else x
+
+
+def reconstruct(a: "Sense", y: np.ndarray, dims, reg: str, lam: float, iters: int, tol: float = 0.0,
+                step_scale: float = 0.9):
+    """Full-coil min 0.5||A x - y||^2 + g(x) (solvers.py:434-500): l2 -> cg_normal
+    (solvers.py:232-257, stop at tol * ||A^H y||), l1-wavelet -> FISTA with L from the power
+    iteration and the composite objective recorded per iteration.  Returns (x, iterations,
+    history, coil transforms)."""
+    n0 = a.counter.counts.get("coil_transform", 0)
+    D = int(np.prod(dims))
+    x0 = np.zeros(D, dtype=np.complex128)
+    if reg == "l2":
+        b = a.adjoint(y)
+        x, it, hist = cg(lambda u: a.adjoint(a.forward(u)) + lam * u, b, x0, iters, tol * float(np.linalg.norm(b)),
+                         full=True)
+    else:
+        a.counter.depth += 1
+        L = power_max_eig(a.normal, D) / step_scale
+        a.counter.depth -= 1
+
+        def objective(v):
+            a.counter.depth += 1
+            r = a.forward(v) - y
+            a.counter.depth -= 1
+            return 0.5 * float(np.linalg.norm(r) ** 2) + wavelet_l1(v, dims, lam)
+
+        x, it, hist = fista(lambda v: a.adjoint(a.forward(v) - y), lambda v, st: wavelet_prox(v, dims, st, lam),
+                            L, x0, iters, tol, objective=objective, full=True)
+    return x, it, hist, a.counter.counts.get("coil_transform", 0) - n0
+
+
+def gfactor_montecarlo(recon, a_full: "Sense", a_under: "Sense", x_true: np.ndarray, noise_sigma: float,
+                       trials: int, R: float, seed: int, support_rel_threshold: float = 1e-3):
+    """Pseudo-replica inverse g-factor (metrics.py:157-211): per trial i, noise from
+    seed_stream(seed, i) (full data first, then undersampled), both reconstructed by recon(op, y);
+    inverse_g = std_full sqrt(R) / std_under on the support (|x| > thr max|x|) where the
+    undersampled std is not degenerate.  Returns (inverse_g, mask)."""
+    if trials < 2:
+        raise ValueError("need at least 2 trials")
+    clean_full = a_full.forward_unweighted(x_true)
+    clean_under = a_under.forward_unweighted(x_true)
+    scale = noise_sigma / math.sqrt(2.0)
+    rf = np.empty((trials, x_true.size), dtype=np.complex128)
+    ru = np.empty_like(rf)
+    for i in range(trials):
+        g = seed_stream(seed, i)
+        n_full = scale * (g.standard_normal(clean_full.shape) + 1j * g.standard_normal(clean_full.shape))
+        n_under = scale * (g.standard_normal(clean_under.shape) + 1j * g.standard_normal(clean_under.shape))
+        rf[i] = recon(a_full, a_full.weight_data(clean_full + n_full))
+        ru[i] = recon(a_under, a_under.weight_data(clean_under + n_under))
+    sf, su = np.std(rf, axis=0), np.std(ru, axis=0)
+    mag = np.abs(x_true)
+    mask = (mag > support_rel_threshold * mag.max()) & ~(su <= np.finfo(float).tiny)
+    inv = np.zeros(x_true.size)
+    inv[mask] = sf[mask] * math.sqrt(R) / su[mask]
+    return inv, mask
 
 
 # --------------------------------------------------------------------------
@@ -677,6 +744,8 @@ class ReconResult:
     counts: dict
     diverged: bool
     lipschitz: float
+    init_count: int = 0
+    per_outer_counts: list = field(default_factory=list)
 
 
 def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, *,
@@ -684,12 +753,18 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
                          seed: int = 0, weights=None, rademacher_scale: float = 1.0,
                          solver: str = "fista", reg: str = "l1-wavelet",
                          step_scale: float = 0.9, distribution: str = "rademacher",
-                         cg_iters: int = 8, pdhg_ratio: float = 1.0) -> ReconResult:
+                         cg_iters: int = 8, pdhg_ratio: float = 1.0, tol: float = 0.0,
+                         reuse_step_size: bool = True, use_init: bool = False,
+                         init_iters: int = 100) -> ReconResult:
     """Outer true-gradient + fresh sketch + warm-started inner solve (coil_sketch.py:220-306).
 
     make_kernel() builds the Fourier kernel (shared by full and sketched ops).
     reg: 'l1-wavelet' (FISTA), 'l2' (CG, coil_sketch.py:182-191) or 'l1-tv' (PDHG with an
     inner CG of cg_iters steps, coil_sketch.py:200-216).
+    tol: FISTA relative-change stop of the inner solves (solvers.py:300, passed through
+    coil_sketch.py:171-178); reuse_step_size=False re-estimates the Lipschitz constant every
+    outer (coil_sketch.py:281); use_init runs the classical-sketch solve of
+    coil_sketch.py:148-159, 268-272 (init_iters = SolverConfig.max_iters) before the loop.
     """
     d0, m0, _, _ = coil_compress_svd(data, maps, c_hat0)
     counter = Counter()
@@ -716,6 +791,14 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
     objs = []
     diverged = False
     L = None
+    init_count = 0
+    if use_init:
+        before = counter.counts.get("coil_transform", 0)
+        S0 = gen_sketch_matrix(v + s, v, s, c_hat0, child_seed(seed, 0), distribution, rademacher_scale)
+        x = classical_sketch_solve(a, y, S0, m0, kern, weights, counter, dims, lam, reg, solver, init_iters,
+                                   tol, step_scale)
+        init_count = counter.counts.get("coil_transform", 0) - before
+    per_outer = []
     for t in range(1, outer + 1):
         dvec = a.adjoint(a.forward(x) - y)
         S = gen_sketch_matrix(v + s, v, s, c_hat0, child_seed(seed, t), distribution,
@@ -727,7 +810,7 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
             return a_s.adjoint(a_s.forward(u))
 
         if solver == "fista":
-            if L is None:
+            if L is None or not reuse_step_size:
                 counter.depth += 1
                 L = power_max_eig(normal_s, D) / step_scale
                 counter.depth -= 1
@@ -739,7 +822,7 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
                 return wavelet_prox(vv, dims, st, lam) if reg == "l1-wavelet" else (
                     vv / (1.0 + st * lam) if lam else vv.copy())
 
-            x = fista(grad, prox, L, anchor, inner)
+            x = fista(grad, prox, L, anchor, inner, tol)
         elif solver == "cg":
             b = -dvec - lam * anchor
             delta = cg(lambda u: normal_s(u) + lam * u, b, np.zeros(D, dtype=np.complex128), inner)
@@ -751,8 +834,36 @@ def coil_sketching_recon(data: np.ndarray, maps: np.ndarray, dims, make_kernel, 
         finite = bool(np.all(np.isfinite(x)))
         obj = objective(x) if finite else math.inf
         objs.append(obj)
+        per_outer.append(counter.counts.get("coil_transform", 0))
         if not finite or obj > 10.0 * obj0:
             diverged = True
             break
     return ReconResult(np.where(np.isfinite(x), x, 0.0), objs, dict(counter.counts), diverged,
-                       float(L) if L is not None else float("nan"))
+                       float(L) if L is not None else float("nan"), init_count, per_outer)
+
+
+def classical_sketch_solve(a: "Sense", y: np.ndarray, S: np.ndarray, m0: np.ndarray, kern, weights, counter,
+                           dims, lam: float, reg: str, solver: str, iters: int, tol: float,
+                           step_scale: float) -> np.ndarray:
+    """One-shot min 0.5||S A x - S y||^2 + g(x) (coil_sketch.py:148-159) through reconstruct
+    (solvers.py:434-500): the sketched data is S applied per sample (sketching.py:106-109)."""
+    a_s = Sense(S @ m0, kern, weights, counter)
+    y_s = (S @ y.reshape(m0.shape[0], -1)).ravel()
+    D = int(np.prod(dims))
+    x0 = np.zeros(D, dtype=np.complex128)
+    if solver == "cg":
+        b = a_s.adjoint(y_s)
+        return cg(lambda u: a_s.adjoint(a_s.forward(u)) + lam * u, b, x0, iters,
+                  tol * float(np.linalg.norm(b)))
+    counter.depth += 1
+    L = power_max_eig(lambda u: a_s.adjoint(a_s.forward(u)), D) / step_scale
+    counter.depth -= 1
+
+    def grad(z):
+        return a_s.adjoint(a_s.forward(z) - y_s)
+
+    def prox(vv, st):
+        return wavelet_prox(vv, dims, st, lam) if reg == "l1-wavelet" else (
+            vv / (1.0 + st * lam) if lam else vv.copy())
+
+    return fista(grad, prox, L, x0, iters, tol)

@@ -67,6 +67,10 @@ SIGNATURES = {
     "sr_nufft_adjoint": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                          _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_partial_blocks": [_ll],
+    "sr_cart3_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_cart3_forward": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp],
+    "sr_cart3_adjoint": [_vp, _ll, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sr_cart3_partial_blocks": [_ll, _i],
     "sr_nufft_plan_geom": [_vp, _ll, _i, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "sr_nufft_plan_permute": [_vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp],
     "sr_nufft_plan_create": [_vp, _ll, _i, _vp, C.c_double, _i, _i, _vp, _vp],

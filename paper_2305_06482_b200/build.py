@@ -33,8 +33,18 @@ def _sources():
     return sorted(srcs, key=lambda p: (-p.stat().st_size * (3 if "_inst_" in p.name else 1), p.name))
 
 
+FLAGS_FILE = OUT_DIR / "build_flags.txt"
+
+
+def _flag_line() -> str:
+    return " ".join([NVCC, *ARCH, *FLAGS])
+
+
 def _needs_build() -> bool:
     if not LIB.exists():
+        return True
+    # a library built with other flags (e.g. an SR_NVCC_EXTRA measurement knob) is rebuilt
+    if not FLAGS_FILE.exists() or FLAGS_FILE.read_text().strip() != _flag_line():
         return True
     t = LIB.stat().st_mtime
     deps = list(CSRC.glob("*")) + list(INCLUDE.glob("*.h"))
@@ -68,6 +78,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    FLAGS_FILE.write_text(_flag_line() + "\n")
     return LIB
 
 

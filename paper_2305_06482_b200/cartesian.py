@@ -86,7 +86,11 @@ class CartesianKernel:
         self._replicas: dict[int, "CartesianKernel"] = {}
 
     @classmethod
-    def from_points(cls, dims, points) -> "CartesianKernel":
+    def from_points(cls, dims, points):
+        """Kernel for one trajectory; a 3-D grid gets the grid-pipeline Cartesian3DKernel."""
+        if len(tuple(dims)) == 3:
+            from .cartesian3d import Cartesian3DKernel
+            return Cartesian3DKernel(dims, points)
         return cls(dims, [cartesian_plan(tuple(dims), points)])
 
     # ------------------------------------------------------------------ device
@@ -139,15 +143,24 @@ class CartesianKernel:
                   dv.ptr(self.maskT) + b0 * self.mask_bstride, self.mask_bstride, dv.ptr(out) + xo,
                   dv.ptr(ws), b1 - b0, ncoils, self.ny, self.nx, None, None, None, 0, stream)
 
-    def normal_host(self, maps, x_host, out_host, *, chunks: int = 8, buffers=None, lanes: int = 1):
+    def normal_host(self, maps, x_host, out_host, *, chunks: int = 8, buffers=None, lanes: int = 1,
+                    overlap_prev: bool = False, sync: bool = False):
         """A^H A on HOST (pinned) buffers, pipelined: slice chunks are copied in, applied and
         copied out so PCIe transfers overlap the K1 launches.  Chunk i runs its K1 on compute
         lane i % lanes (own stream and workspace), so two small-grid K1 launches share the GPU.
 
-        x_host/out_host: pinned (B, D) complex64 CPU tensors.  Returns out_host (synchronised).
+        x_host/out_host: pinned (B, D) complex64 CPU tensors.  The call is asynchronous: it returns
+        out_host once the copies are enqueued and makes the current stream wait for them, so the
+        caller must synchronise (``torch.cuda.current_stream().synchronize()``, or pass
+        ``sync=True``) before reading out_host or rewriting x_host.
         `chunks` = number of equal chunks, or a sequence of slice counts summing to B (a small
         last chunk shortens the pipeline drain: its K1 + D2H are all that follow the last H2D).
         `buffers` = (x_dev, out_dev) device staging tensors to reuse across calls.
+        `overlap_prev` = True lets this call's host-to-device copies start while the previous
+        call's last chunks still compute (they wait only for the previous call's K1 events on
+        the same staging buffers, not for the current stream).  Only valid when this kernel
+        instance owns `buffers` exclusively: no other stream work may read or write them
+        between calls.  Default False: the copies wait for the current stream.
         """
         import torch
         if x_host.device.type != "cpu" or out_host.device.type != "cpu":
@@ -186,7 +199,7 @@ class CartesianKernel:
         # pipeline: this call's copies start while the previous call's last chunks compute and
         # copy back (same chunking and staging buffers: per-chunk events; otherwise a full wait).
         prev = getattr(self, "_host_prev", None)
-        if prev is not None and prev[0] == bounds and prev[1] is xd:
+        if overlap_prev and prev is not None and prev[0] == bounds and prev[1] is xd:
             for ev in prev[2]:
                 s_in.wait_event(ev)
         else:
@@ -213,6 +226,8 @@ class CartesianKernel:
         cur.wait_stream(s_out)
         for st in s_k[:lanes]:
             cur.wait_stream(st)
+        if sync:
+            s_out.synchronize()
         return out_host
 
     def partial_shape(self, ncoils: int) -> tuple:

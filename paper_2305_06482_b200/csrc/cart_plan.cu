@@ -92,6 +92,14 @@ int sr_cart_plan_create(const double* pts, const long long* counts, int batch, i
     ptotal += counts[b];
   }
   if (ptotal > 0 && !pts) return SR_EINVAL;
+  // Trajectory.validate_for (linops.py:130-140): every coordinate in [-n/2, n/2) per axis
+  for (long long i = 0; i < ptotal; ++i) {
+    for (int a = 0; a < ndim; ++a) {
+      const double n = (double)(ndim == 2 && a == 0 ? ny : nx);
+      const double v = pts[i * ndim + a];
+      if (!(v >= -n / 2) || !(v < n / 2)) return SR_EINVAL;
+    }
+  }
   const long long D = (long long)ny * nx;
   const int nblk = (nx + cb - 1) / cb;
   // per distinct plan: tables in trajectory order

@@ -36,7 +36,10 @@ __global__ void k_plan_geom(const double* __restrict__ pts, long long N, int nd,
   long long binid = 0, local = 0;
   for (int a = 0; a < nd; ++a) {
     const int n = pd.n[a], g = pd.g[a];
-    const double u = pts[i * nd + a] * ((double)g / (double)n);
+    // Trajectory.validate_for (linops.py:130-140): coordinates in [-n/2, n/2)
+    const double pv = pts[i * nd + a];
+    if (!(pv >= -0.5 * n) || !(pv < 0.5 * n)) atomicExch(err, 1);
+    const double u = pv * ((double)g / (double)n);
     const double b = ceil(u - (double)w / 2.0);
     const double d = u - b;
     float t = __double2float_rn(d);
@@ -370,7 +373,7 @@ int sr_nufft_plan_create(const double* pts, long long nsamples, int ndim, const 
       rc = SR_ECUDA;
       break;
     }
-    if (herr) { rc = SR_EINVAL; break; }  // float32 support decisions could not be aligned
+    if (herr) { rc = SR_EINVAL; break; }  // out-of-range coordinate, or float32 support decisions not aligned
     p->nchunks = (long long)last_pos + last_flag;
     if (cudaMalloc(&p->chunks, sizeof(int) * 5 * p->nchunks) != cudaSuccess) { rc = SR_ECUDA; break; }
     k_plan_chunks<<<nbk, T, 0, st>>>(skey, flag, cpos, N, bnd, ndim, p->binsize, nbins[0], nbins[1], nbins[2],

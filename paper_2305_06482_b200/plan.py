@@ -38,7 +38,7 @@ def grid2d(dims: tuple[int, ...]) -> tuple[int, int]:
         return 1, int(dims[0])
     if len(dims) == 2:
         return int(dims[0]), int(dims[1])
-    raise NotImplementedError("Cartesian kernels are 1-D/2-D; 3-D data is readout-decoupled first")
+    raise NotImplementedError("the 2-D Cartesian kernels take 1-D/2-D grids; 3-D grids use Cartesian3DKernel")
 
 
 @dataclass(frozen=True)

@@ -169,7 +169,7 @@ def main():
 
     # --- end-to-end coil-sketched reconstructions (coil_sketch.py:220-330)
     def recon_case(name, dims, C, chat0, v, s, lam, T, K, scale, solver="fista", kind="l1-wavelet",
-                   nufft=None):
+                   nufft=None, solver_cfg=None, reuse=True, use_init=False):
         shape = lo.GridShape(dims)
         maps = smooth_maps(g, dims, C)
         img = np.zeros(dims, complex)
@@ -201,9 +201,9 @@ def main():
         try:
             reg = so.make_regularizer(kind, lam, shape)
             cfg = cs.CoilSketchConfig(chat0, sk.SketchConfig(v + s, v, s, "rademacher", 0), reg, T, K,
-                                      solver=solver)
+                                      solver=solver, reuse_step_size=reuse, use_init=use_init)
             rep = cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps), cfg,
-                                          weights=weights)
+                                          weights=weights, solver_cfg=solver_cfg)
         finally:
             cs.gen_sketch_matrix = orig_gen
             fm.make_fourier_kernel = orig_mk
@@ -216,7 +216,12 @@ def main():
                          diverged=np.array(rep.diverged),
                          weights=np.zeros(0) if weights is None else weights.w,
                          oversamp=np.array(0.0 if nufft is None else nufft[2]),
-                         width=np.array(0 if nufft is None else nufft[3]))
+                         width=np.array(0 if nufft is None else nufft[3]),
+                         tol=np.array(0.0 if solver_cfg is None else solver_cfg.tol),
+                         max_iters=np.array(100 if solver_cfg is None else solver_cfg.max_iters),
+                         reuse=np.array(reuse), use_init=np.array(use_init),
+                         init_counts=np.array(rep.init_coil_transforms),
+                         per_outer_counts=np.array([r.coil_transforms for r in rep.per_outer]))
 
     recon_case("recon_cart", (32, 32), 8, 8, 2, 2, 1e-3, 3, 4, 1.0 / np.sqrt(12))
     recon_case("recon_cart_pm1", (40, 32), 6, 6, 2, 1, 5e-3, 2, 5, 1.0)
@@ -316,6 +321,80 @@ def main():
                                    beta_min=np.array(0.25 / L), iters=np.array(8), seed=np.array(3),
                                    x=res2.x.values, iterations=np.array(res2.iterations_run),
                                    counts=np.array(res2.coil_transform_count), unused_n0=np.array(n0))
+
+    # --- round 2 (appended last: earlier fixtures keep their RNG stream)
+    # 3-D Cartesian mask SENSE operator (linops.py:332-364 on a 3-D grid), duplicated bins
+    dims = (12, 10, 8)
+    shape = lo.GridShape(dims)
+    pts = random_mask_points(g, dims, 0.3)
+    pts = np.concatenate([pts, pts[:7]], axis=0)
+    traj = lo.Trajectory(pts, "cartesian-mask")
+    maps = smooth_maps(g, dims, 4)
+    a = fm.build_sense(fm.SensitivityMaps(shape, maps), traj)
+    xx = crandn(g, shape.size)
+    yy = crandn(g, 4 * traj.n_points)
+    S = sk.gen_sketch_matrix(sk.SketchConfig(3, 2, 1, "rademacher", rng.child_seed(0, 2)), 4)
+    a_s = sk.build_sketched_operator(a, S)
+    out["sense_cart3d"] = dict(dims=np.array(dims), points=pts, maps=maps, x=xx, y=yy, Ax=a.forward(xx),
+                               AHy=a.adjoint(yy), AHAx=a.adjoint(a.forward(xx)), S=S.mat,
+                               AsHAsx=a_s.adjoint(a_s.forward(xx)))
+    # Algorithm 1 on a 3-D Cartesian mask; FISTA early stopping (tol > 0, solvers.py:300);
+    # per-outer step sizes (reuse_step_size=False, coil_sketch.py:281); classical-sketch init
+    # (use_init, coil_sketch.py:148-159, 268-272)
+    recon_case("recon_cart3d", (16, 12, 10), 4, 4, 2, 1, 1e-3, 2, 3, 1.0 / np.sqrt(12))
+    recon_case("recon_cart_tol", (32, 24), 6, 6, 2, 2, 2e-3, 3, 12, 1.0,
+               solver_cfg=so.SolverConfig(tol=0.02))
+    recon_case("recon_cart_noreuse", (24, 32), 6, 6, 2, 2, 1e-3, 3, 4, 1.0 / np.sqrt(12), reuse=False)
+    recon_case("recon_cart_init", (24, 24), 6, 6, 2, 2, 1e-3, 2, 3, 1.0,
+               solver_cfg=so.SolverConfig(max_iters=6, tol=0.0), use_init=True)
+    # full-coil reconstruct(): l1-wavelet -> FISTA, l2 -> CG (solvers.py:434-500), incl. tol stops
+    dims = (24, 20)
+    shape = lo.GridShape(dims)
+    maps = smooth_maps(g, dims, 5)
+    pts = random_mask_points(g, dims, 0.4)
+    traj = lo.Trajectory(pts, "cartesian-mask")
+    a = fm.build_sense(fm.SensitivityMaps(shape, maps), traj)
+    grids = np.meshgrid(*[np.linspace(-1, 1, n, endpoint=False) for n in dims], indexing="ij")
+    img = np.zeros(dims, complex)
+    for _ in range(3):
+        c = g.uniform(-0.4, 0.4, 2); ax = g.uniform(0.15, 0.5, 2)
+        img += g.uniform(0.2, 1.0) * (sum(((gg - cc) / aa) ** 2 for gg, cc, aa in zip(grids, c, ax)) <= 1)
+    clean = a.forward(img.ravel())
+    y = clean + (g.standard_normal(clean.shape) + 1j * g.standard_normal(clean.shape)) * 0.01 * np.abs(clean).max()
+    res_f = so.reconstruct(a, y, so.make_regularizer("l1-wavelet", 1e-3, shape),
+                           so.SolverConfig(max_iters=12, tol=0.0, record_history=True))
+    res_ft = so.reconstruct(a, y, so.make_regularizer("l1-wavelet", 1e-3, shape),
+                            so.SolverConfig(max_iters=40, tol=3e-3))
+    res_c = so.reconstruct(a, y, so.make_regularizer("l2", 1e-2, shape), so.SolverConfig(max_iters=10, tol=0.0,
+                                                                                         record_history=True))
+    res_ct = so.reconstruct(a, y, so.make_regularizer("l2", 1e-2, shape), so.SolverConfig(max_iters=50, tol=1e-3))
+    out["solve_full"] = dict(dims=np.array(dims), points=pts, maps=maps, y=y,
+                             fista_x=res_f.x.values, fista_hist=res_f.objective_history,
+                             fista_counts=np.array(res_f.coil_transform_count),
+                             fista_tol_x=res_ft.x.values, fista_tol_iters=np.array(res_ft.iterations_run),
+                             cg_x=res_c.x.values, cg_hist=res_c.objective_history,
+                             cg_counts=np.array(res_c.coil_transform_count),
+                             cg_tol_x=res_ct.x.values, cg_tol_iters=np.array(res_ct.iterations_run))
+    # pseudo-replica inverse g-factor with a CG-l2 reconstruction (metrics.py:157-211)
+    import sketchrecon.metrics as met
+    dims = (20, 16)
+    shape = lo.GridShape(dims)
+    maps = smooth_maps(g, dims, 4)
+    full_pts = np.argwhere(np.ones(dims, bool)).astype(np.float64) - np.array([n // 2 for n in dims])
+    under_pts = full_pts[(full_pts[:, 0] % 2 == 0) | (np.abs(full_pts[:, 0]) < 3)]
+    a_full = fm.build_sense(fm.SensitivityMaps(shape, maps), lo.Trajectory(full_pts, "cartesian-mask"))
+    a_under = fm.build_sense(fm.SensitivityMaps(shape, maps), lo.Trajectory(under_pts, "cartesian-mask"))
+    img = np.zeros(dims, complex)
+    grids = np.meshgrid(*[np.linspace(-1, 1, n, endpoint=False) for n in dims], indexing="ij")
+    img += 1.0 * ((grids[0] / 0.7) ** 2 + (grids[1] / 0.6) ** 2 <= 1)
+    reg2 = so.make_regularizer("l2", 1e-3, shape)
+    recon = lambda op, yy: so.reconstruct(op, yy, reg2, so.SolverConfig(max_iters=8, tol=0.0)).x  # noqa: E731
+    R = full_pts.shape[0] / under_pts.shape[0]
+    gm = met.gfactor_montecarlo(recon, a_full, a_under, lo.Image(shape, img.ravel()), 0.05, 4, R, 11)
+    out["gfactor"] = dict(dims=np.array(dims), maps=maps, full_points=full_pts, under_points=under_pts,
+                          truth=img.ravel(), sigma=np.array(0.05), trials=np.array(4), R=np.array(R),
+                          seed=np.array(11), lam=np.array(1e-3), iters=np.array(8),
+                          inverse_g=gm.inverse_g, mask=gm.mask)
 
     only = set(sys.argv[1:])
     written = []

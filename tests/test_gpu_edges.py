@@ -215,3 +215,33 @@ def test_tsqr_r_matches_lapack(cuda, S, N, C):
     for s in range(S):
         ref = np.linalg.qr(A[s], mode="r")
         np.testing.assert_allclose(R[s], ref, rtol=0, atol=1e-10 * np.abs(ref).max())
+
+
+def test_c_abi_plans_reject_out_of_range_coordinates(cuda):
+    """sr_cart_plan_create / sr_nufft_plan_create return SR_EINVAL (ValueError) for a coordinate
+    outside [-n/2, n/2), as Trajectory.validate_for (linops.py:130-140) rejects it, instead of
+    wrapping it modulo n."""
+    import ctypes
+    from paper_2305_06482_b200 import _device as dv
+    from paper_2305_06482_b200 import _lib
+    dims = (32, 40)
+    cdims = (ctypes.c_int * 2)(*dims)
+    for bad in ([16.0, 0.0], [-17.0, 0.0], [0.0, 20.0], [0.0, float("nan")]):
+        pts = np.array([[0.0, 0.0], bad], dtype=np.float64)
+        counts = (ctypes.c_longlong * 1)(2)
+        plan = ctypes.c_void_p()
+        with pytest.raises(ValueError):
+            _lib.call("sr_cart_plan_create", pts.ctypes.data, counts, 1, 2, cdims, 0, ctypes.byref(plan), dv.stream())
+        nplan = ctypes.c_void_p()
+        with pytest.raises(ValueError):
+            _lib.call("sr_nufft_plan_create", pts.ctypes.data, 2, 2, cdims, 2.0, 4, 0, ctypes.byref(nplan),
+                      dv.stream())
+    # the edge values themselves are accepted
+    pts = np.array([[-16.0, -20.0], [15.0, 19.0]], dtype=np.float64)
+    counts = (ctypes.c_longlong * 1)(2)
+    plan = ctypes.c_void_p()
+    _lib.call("sr_cart_plan_create", pts.ctypes.data, counts, 1, 2, cdims, 0, ctypes.byref(plan), dv.stream())
+    _lib.call("sr_cart_plan_destroy", plan)
+    nplan = ctypes.c_void_p()
+    _lib.call("sr_nufft_plan_create", pts.ctypes.data, 2, 2, cdims, 2.0, 4, 0, ctypes.byref(nplan), dv.stream())
+    _lib.call("sr_nufft_plan_destroy", nplan)

@@ -504,12 +504,22 @@ def test_normal_host_pipelined_matches_device(cuda):
           .pin_memory() for _ in range(6)]
     outs = [torch.empty(B, D, dtype=torch.complex64).pin_memory() for _ in range(6)]
     for xi, oi in zip(xs, outs):
-        kern.normal_host(maps, xi, oi, chunks=3, buffers=stage)
+        kern.normal_host(maps, xi, oi, chunks=3, buffers=stage, overlap_prev=True)
     torch.cuda.synchronize()
     for xi, oi in zip(xs, outs):
         r = torch.empty(B, D, dtype=torch.complex64, device="cuda")
         kern.normal(maps, xi.cuda(), r)
         assert rel(oi.numpy(), r.cpu().numpy()) < 1e-6
+    # default (no overlap): work on the current stream that reads the staging input between two
+    # calls sees the first call's input, not the second call's (the H2D waits for the stream)
+    seen = torch.empty(B, D, dtype=torch.complex64, device="cuda")
+    o1 = torch.empty(B, D, dtype=torch.complex64).pin_memory()
+    kern.normal_host(maps, xs[0], o1, chunks=3, buffers=stage)
+    torch.cuda._sleep(2_000_000)  # keep the stream busy so a racing H2D would land first
+    seen.copy_(stage[0])
+    kern.normal_host(maps, xs[1], o1, chunks=3, buffers=stage, sync=True)
+    torch.cuda.synchronize()
+    assert torch.equal(seen.cpu(), xs[0])
 
 
 @pytest.mark.parametrize("binned", [True, False])

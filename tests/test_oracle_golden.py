@@ -162,3 +162,70 @@ def test_chunked_gridded_kernel_equals_gridded_kernel():
     k = O.ChunkedGriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]), chunk=7)
     assert rel(k.apply(g["batch"]), g["fwd"]) < TOL
     assert rel(k.apply_adjoint(g["y"]), g["adj"]) < TOL
+
+
+def test_cartesian_sense_3d():
+    """3-D Cartesian mask SENSE (linops.py:332-364 on a 3-D grid), duplicated bins."""
+    g = golden("sense_cart3d")
+    dims = tuple(int(n) for n in g["dims"])
+    k = O.CartesianKernel(dims, g["points"])
+    a = O.Sense(g["maps"], k)
+    assert rel(a.forward(g["x"]), g["Ax"]) < TOL
+    assert rel(a.adjoint(g["y"]), g["AHy"]) < TOL
+    assert rel(a.normal(g["x"]), g["AHAx"]) < TOL
+    assert rel(O.Sense(g["S"] @ g["maps"], k).normal(g["x"]), g["AsHAsx"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["recon_cart3d", "recon_cart_tol", "recon_cart_noreuse", "recon_cart_init"])
+def test_recon_options(name):
+    """Algorithm 1 with a 3-D mask, FISTA early stopping (tol > 0), per-outer step sizes and the
+    classical-sketch initialisation (coil_sketch.py:148-159, 220-306; solvers.py:300)."""
+    g = golden(name)
+    dims = tuple(int(n) for n in g["dims"])
+    res = O.coil_sketching_recon(g["data"], g["maps"], dims, _kernel_for(g), c_hat0=int(g["chat0"]),
+                                 v=int(g["v"]), s=int(g["s"]), lam=float(g["lam"]), outer=int(g["outer"]),
+                                 inner=int(g["inner"]), seed=0, rademacher_scale=float(g["scale"]),
+                                 tol=float(g["tol"]), reuse_step_size=bool(g["reuse"]),
+                                 use_init=bool(g["use_init"]), init_iters=int(g["max_iters"]))
+    assert rel(res.x_final, g["x_final"]) < 1e-9
+    np.testing.assert_allclose(res.objectives, g["objectives"], rtol=1e-9)
+    assert res.counts["coil_transform"] == int(g["counts"])
+    assert res.per_outer_counts == list(g["per_outer_counts"])
+    assert res.init_count == int(g["init_counts"])
+    if float(g["tol"]) > 0:
+        assert int(g["counts"]) < int(g["expected"])  # the early stop fired
+
+
+def test_full_coil_reconstruct():
+    """reconstruct(): l1-wavelet -> FISTA, l2 -> CG, fixed count and tol stops (solvers.py:232-500)."""
+    g = golden("solve_full")
+    dims = tuple(int(n) for n in g["dims"])
+    k = O.CartesianKernel(dims, g["points"])
+    a = O.Sense(g["maps"], k)
+    x, it, hist, cnt = O.reconstruct(a, g["y"], dims, "l1-wavelet", 1e-3, 12)
+    assert rel(x, g["fista_x"]) < 1e-9 and cnt == int(g["fista_counts"])
+    np.testing.assert_allclose(hist, g["fista_hist"], rtol=1e-9)
+    x, it, _, _ = O.reconstruct(a, g["y"], dims, "l1-wavelet", 1e-3, 40, tol=3e-3)
+    assert rel(x, g["fista_tol_x"]) < 1e-9 and it == int(g["fista_tol_iters"])
+    x, it, hist, cnt = O.reconstruct(a, g["y"], dims, "l2", 1e-2, 10)
+    assert rel(x, g["cg_x"]) < 1e-9 and cnt == int(g["cg_counts"])
+    np.testing.assert_allclose(hist, g["cg_hist"], rtol=1e-9)
+    x, it, _, _ = O.reconstruct(a, g["y"], dims, "l2", 1e-2, 50, tol=1e-3)
+    assert rel(x, g["cg_tol_x"]) < 1e-9 and it == int(g["cg_tol_iters"])
+
+
+def test_gfactor_montecarlo():
+    """Pseudo-replica inverse g-factor with a CG-l2 recon (metrics.py:157-211)."""
+    g = golden("gfactor")
+    dims = tuple(int(n) for n in g["dims"])
+    a_full = O.Sense(g["maps"], O.CartesianKernel(dims, g["full_points"]))
+    a_under = O.Sense(g["maps"], O.CartesianKernel(dims, g["under_points"]))
+    lam, iters = float(g["lam"]), int(g["iters"])
+
+    def recon(op, y):
+        return O.reconstruct(op, y, dims, "l2", lam, iters)[0]
+
+    inv, mask = O.gfactor_montecarlo(recon, a_full, a_under, g["truth"], float(g["sigma"]), int(g["trials"]),
+                                     float(g["R"]), int(g["seed"]))
+    np.testing.assert_array_equal(mask, g["mask"])
+    assert rel(inv, g["inverse_g"]) < 1e-9
