@@ -150,8 +150,6 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
     """
     if cfg.c_hat0 > data.n_coils:
         raise ValueError(f"c_hat0 = {cfg.c_hat0} exceeds the {data.n_coils} available coils")
-    if not cfg.reuse_step_size:
-        raise NotImplementedError("reuse_step_size=False is not implemented on the device path")
     kind = _reg_kind(cfg.reg)
     if compress not in ("device", "lapack"):
         raise ValueError(f"compress must be 'device' or 'lapack', got {compress!r}")
@@ -167,8 +165,6 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
         a = SenseOperator(maps0, data0.traj, weights, method=method, kernel=kernel)
         y = dv.c64(a.measurement_vector(data0)).view(1, cfg.c_hat0, a.n_points)
     solver_cfg = solver_cfg or SolverConfig(tol=0.0)
-    if solver_cfg.tol != 0.0:
-        raise NotImplementedError("the device engine runs the fixed-count inner loop (tol = 0)")
     ypad = torch.zeros(1, cfg.c_hat0, a.kernel.nmax, dtype=torch.complex64, device=y.device)
     ypad[:, :, : a.n_points] = y
     init_count = 0
@@ -187,7 +183,11 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
                               wavelet_levels=getattr(cfg.reg.transform, "levels", None), counter=a.counter,
                               pdhg_ratio=solver_cfg.pdhg_sigma_tau_ratio, cg_iters=solver_cfg.inner_cg_iters)
     ref = None if x_ref is None else dv.c64(x_ref.values).view(1, -1)
-    res = eng.run(cfg.outer_iters, cfg.inner_iters, x0=x0_dev, x_ref=ref)
+    # the reference passes tol to the FISTA / PDHG sub-solvers; its CG sub-solver always runs
+    # the full budget (coil_sketch.py:182-191)
+    tol = solver_cfg.tol if cfg.solver in ("fista", "pdhg") else 0.0
+    res = eng.run(cfg.outer_iters, cfg.inner_iters, x0=x0_dev, x_ref=ref, tol=tol,
+                  reuse_step_size=cfg.reuse_step_size)
     report = ReconReport(x_final=Image(maps.shape, dv.to_numpy128(res.x[0])), energy_fraction=energy,
                          init_coil_transforms=init_count)
     for t in range(len(res.objectives)):

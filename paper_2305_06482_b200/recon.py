@@ -219,12 +219,21 @@ class SketchedReconEngine:
                       self.D, self.D, self.B, st)
         return lam
 
-    def _fista(self, smaps, inner: int):
-        """Warm-started FISTA on the anchored sub-problem (coil_sketch.py:192-199, solvers.py:284-301)."""
+    def _fista(self, smaps, inner: int, tol: float = 0.0):
+        """Warm-started FISTA on the anchored sub-problem (coil_sketch.py:192-199, solvers.py:284-301).
+
+        tol > 0 (B = 1): the reference's relative-change stop `||x_new - x|| / ||x|| < tol`
+        (solvers.py:296-301), evaluated with the fixed-order device reductions and one host
+        read per inner iteration.  Returns the number of inner iterations run."""
         self.x.copy_(self.anchor)
         self.z.copy_(self.anchor)
         t_k = 1.0
-        for _ in range(inner):
+        if tol > 0.0:
+            xold = torch.empty_like(self.x)
+        it = 0
+        for it in range(1, inner + 1):
+            if tol > 0.0:
+                xold.copy_(self.x)
             self.counter.add("coil_transform", 2 * self.chat)
             # v = z - step * (A_s^H A_s (z - anchor) + d)
             self._normal(smaps, self.z, self.v, anchor=self.anchor, coef=self.fcoef, u=self.z, d=self.d)
@@ -241,6 +250,9 @@ class SketchedReconEngine:
                 _lincomb(self.z, self.v, self.x, None, 1.0 + beta, -beta, 0.0, self.B, self.D)
                 self.x.copy_(self.v)
             t_k = t_next
+            if tol > 0.0 and self._rel_change_stop(self.x, xold, tol):
+                break
+        return it
 
     def _fista_graphed(self, smaps, inner: int):
         """Replay of the captured inner loop on a persistent sketched-maps buffer."""
@@ -305,7 +317,23 @@ class SketchedReconEngine:
         self._cg_solve(smaps, delta, rhs, lcoef, inner)
         _lincomb(self.x, self.anchor, delta, None, 1.0, 1.0, 0.0, B, D)
 
-    def _pdhg(self, smaps, inner: int):
+    def _rel_change_stop(self, new, old, tol: float) -> bool:
+        """||new - old|| / ||old|| < tol (solvers.py:300, 354) for B = 1, fixed-order device
+        reductions, one host read."""
+        st = dv.stream()
+        if getattr(self, "_tolbuf", None) is None:
+            nparts = _lib.lib().sr_reduce_nparts()
+            self._tolbuf = (torch.empty_like(self.x), torch.empty(1, nparts, 2, dtype=torch.float64, device=self.dev),
+                            torch.empty(2, 2, dtype=torch.float64, device=self.dev))
+        diff, part, rd = self._tolbuf
+        _lincomb(diff, new, old, None, 1.0, -1.0, 0.0, 1, self.D)
+        _lib.call("sr_reduce", 0, dv.ptr(diff), None, self.D, self.D, 1, dv.ptr(part), dv.ptr(rd[0:1]), st)
+        _lib.call("sr_reduce", 0, dv.ptr(old), None, self.D, self.D, 1, dv.ptr(part), dv.ptr(rd[1:2]), st)
+        h = rd[:, 0].cpu().numpy()
+        delta, x_norm = math.sqrt(max(h[0], 0.0)), math.sqrt(max(h[1], 0.0))
+        return x_norm > 0 and delta / x_norm < tol
+
+    def _pdhg(self, smaps, inner: int, tol: float = 0.0):
         """Chambolle-Pock on min_x 0.5||A_s(x - x^t)||^2 + Re<d, x> + lam ||D x||_1 with K = D
         (coil_sketch.py:200-216, solvers.py:315-362): per iteration p = clamp(p + sigma D z, lam),
         v = x - tau D^H p, x' = v + CG_k((A_s^H A_s + I/tau) w = -d - A_s^H A_s (v - x^t)),
@@ -336,12 +364,21 @@ class SketchedReconEngine:
             self._cg_solve(smaps, self.wbuf, self.rhs, shift, self.cg_iters)
             _lincomb(self.xn, self.v, self.wbuf, None, 1.0, 1.0, 0.0, B, D)
             _lincomb(self.z, self.xn, self.x, None, 2.0, -1.0, 0.0, B, D)
+            stop = tol > 0.0 and self._rel_change_stop(self.xn, self.x, tol)
             self.x, self.xn = self.xn, self.x
+            if stop:
+                break
 
     # ------------------------------------------------------------ Algorithm 1
     def run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
-            x_ref: torch.Tensor | None = None) -> EngineResult:
+            x_ref: torch.Tensor | None = None, tol: float = 0.0, reuse_step_size: bool = True) -> EngineResult:
+        """Algorithm 1 (coil_sketch.py:220-306).  tol > 0: FISTA inner solves stop on the relative
+        change (solvers.py:300; B = 1); reuse_step_size=False re-runs the power iteration on
+        every outer's sketched operator (coil_sketch.py:281)."""
         B = self.B
+        tol = float(tol)
+        if tol > 0.0 and (B != 1 or self.solver == "cg"):
+            raise ValueError("inner-solver early stopping (tol > 0) runs FISTA / PDHG one slice at a time")
         t_start = time.perf_counter()
         if x0 is not None:
             self.x.copy_(x0)
@@ -362,7 +399,7 @@ class SketchedReconEngine:
             sk = gen_sketch_matrix(self.sketch.with_seed(child_seed(self.sketch.seed, t)), self.C0)
             self.chat = sk.mat.shape[0]
             smaps = self._sketch(sk.mat)
-            if self.solver == "fista" and lip is None:
+            if self.solver == "fista" and (lip is None or not reuse_step_size):
                 lam_max = self.power_lambda(smaps)
                 lip = lam_max / self.step_scale
                 step = 1.0 / lip
@@ -378,12 +415,12 @@ class SketchedReconEngine:
                 graph = self.use_graph
                 if graph is None:
                     graph = (outer - 2) * inner >= GRAPH_MIN_REPLAYED
-                if graph and t >= 2 and self.reg == "l1-wavelet":
+                if graph and t >= 2 and self.reg == "l1-wavelet" and tol == 0.0:
                     self._fista_graphed(smaps, inner)
                 else:
-                    self._fista(smaps, inner)
+                    self._fista(smaps, inner, tol)
             elif self.solver == "pdhg":
-                self._pdhg(smaps, inner)
+                self._pdhg(smaps, inner, tol)
             else:
                 self._cg(smaps, inner)
             finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1).cpu().numpy()

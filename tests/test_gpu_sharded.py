@@ -1,0 +1,95 @@
+"""The config-4 coil-sharded device engine (coils sharded, image-domain coil
+sum all-reduced, forward_model.py:180 being the sum it replaces) executed end to end: two
+ranks in two processes, gloo on CUDA tensors (this box has one GPU; the collective goes
+through the host, so no rank's kernels wait on another's), against the unsharded engine on
+the same inputs.  Checks the final image, the per-outer objectives, the Lipschitz constant
+and the coil-transform counters (each rank keeps the reference tally of the whole operator)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _engine_inputs(g, dev):
+    from paper_2305_06482_b200 import forward_model as fm
+    from paper_2305_06482_b200 import linops as lo
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    dims = tuple(int(n) for n in g["dims"])
+    shape = lo.GridShape(dims)
+    traj = lo.Trajectory(g["points"], "non-cartesian")
+    kern = GriddedKernel(dims, g["points"], float(g["oversamp"]), int(g["width"]))
+    w = fm.DensityWeights(g["weights"])
+    maps0, data0, _, _ = fm.coil_compress_device(fm.KSpaceData(traj, g["data"]), fm.SensitivityMaps(shape, g["maps"]),
+                                                 int(g["chat0"]))
+    sqrt_w = torch.from_numpy(np.sqrt(w.w)).to(dev, torch.float32)
+    y = (data0 * sqrt_w.to(torch.complex64)).view(1, int(g["chat0"]), -1).contiguous()
+    return dims, kern, maps0.view(1, int(g["chat0"]), -1).contiguous(), y, sqrt_w
+
+
+def _run(g, dev, shard):
+    from paper_2305_06482_b200.recon import SketchedReconEngine
+    from paper_2305_06482_b200.sketching import SketchConfig
+    dims, kern, maps0, y, sqrt_w = _engine_inputs(g, dev)
+    v, s = int(g["v"]), int(g["s"])
+    eng = SketchedReconEngine(kern, maps0, y, dims=dims, sketch=SketchConfig(v + s, v, s, rademacher_scale=float(g["scale"])),
+                              lam=float(g["lam"]), sqrt_w=sqrt_w, shard=shard)
+    res = eng.run(int(g["outer"]), int(g["inner"]))
+    return res
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_06482_b200.parallel_recon import CoilShard
+        g = golden("recon_cones3d")
+        res = _run(g, torch.device("cuda", 0), CoilShard(rank, world))
+        q.put((rank, res.x.cpu().numpy(), np.asarray(res.objectives), float(res.lipschitz[0]),
+               int(res.counts["coil_transform"])))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, repr(e), None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_coil_sharded_engine_world2_matches_unsharded(cuda):
+    import torch.multiprocessing as mp
+    g = golden("recon_cones3d")
+    ref = _run(g, cuda, None)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    xr = ref.x.cpu().numpy()
+    for rank, x, objs, lip, cnt in outs:
+        assert not isinstance(x, str), x
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-5, rank
+        np.testing.assert_allclose(objs, ref.objectives, rtol=1e-5)
+        assert abs(lip - float(ref.lipschitz[0])) < 1e-5 * abs(lip)
+        assert cnt == int(ref.counts["coil_transform"])
+    # both ranks hold the same (replicated) image
+    assert np.array_equal(outs[0][1], outs[1][1])
