@@ -22,11 +22,17 @@ def _axes(dims):
     return [(np.arange(n) - (n - 1) / 2.0) * (2.0 / n) for n in dims]
 
 
-def random_ellipses(dims, n_ellipses: int, rng: np.random.Generator, smooth_phase: bool = True) -> np.ndarray:
+def random_ellipses(dims, n_ellipses: int, rng: np.random.Generator, smooth_phase: bool = True,
+                    planes: tuple[int, int] | None = None) -> np.ndarray:
     """Sum of random ellipses/ellipsoids: intensity U[0.2,1], semi-axes U[0.05,0.4]*FOV,
-    random rotation; times exp(i pi (0.5 x^2 + 0.3 y)) (BASELINE config 0)."""
-    grids = np.meshgrid(*_axes(dims), indexing="ij")
-    img = np.zeros(dims)
+    random rotation; times exp(i pi (0.5 x^2 + 0.3 y)) (BASELINE config 0).
+    planes = (lo, hi) evaluates only those indices of axis 0 (same draws, same values):
+    a rank builds just its slab of a sharded volume."""
+    axes = _axes(dims)
+    if planes is not None:
+        axes[0] = axes[0][planes[0]:planes[1]]
+    grids = np.meshgrid(*axes, indexing="ij")
+    img = np.zeros(tuple(len(a) for a in axes))
     fov = 2.0
     for _ in range(n_ellipses):
         amp = rng.uniform(0.2, 1.0)

@@ -10,9 +10,10 @@ and checks them against the CPU oracle where the oracle finishes.
   torchrun --nproc-per-node N tools/bench_configs.py --config 2     (slices sharded, no collective)
   torchrun --nproc-per-node N tools/bench_configs.py --config 4     (coils sharded, NCCL all-reduce)
 
-Each run prints one JSON line (rank 0).  Times are wall clock around the
-reconstruction call with torch.cuda.synchronize() on both sides (max over ranks
-for N > 1); inputs are seeded synthetic data with the config's shapes.
+Each run prints one JSON line (rank 0); bench.py imports these functions for its `recon`
+and `sharded` objects.  GPU times are CUDA events on the launching stream around the whole
+call (so host work inside the call counts), max over ranks for N > 1; inputs are seeded
+synthetic data with the config's shapes.
 """
 
 from __future__ import annotations
@@ -102,11 +103,13 @@ def run_2d(cfgid: int, with_oracle: bool):
     runs = []
     for _ in range(3):
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         rep = cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps), cfg,
                                       weights=weights, kernel=kern, compress=compress)
+        e1.record()
         torch.cuda.synchronize()
-        runs.append(time.perf_counter() - t0)
+        runs.append(e0.elapsed_time(e1) / 1e3)
     t_gpu = float(np.median(runs))
     if os.environ.get("SR_PROFILE_RECON"):
         from torch.profiler import ProfilerActivity, profile
@@ -134,7 +137,7 @@ def run_2d(cfgid: int, with_oracle: bool):
         line["rel_l2_vs_oracle"] = float(np.linalg.norm(rep.x_final.values - ref.x_final) / np.linalg.norm(ref.x_final))
         line["oracle_objectives"] = ref.objectives
         line["speedup"] = line["cpu_oracle_wall_s"] / t_gpu
-    print(json.dumps(line), flush=True)
+    return line
 
 
 # ----------------------------------------------------------------------------- config 2
@@ -168,12 +171,12 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256, pool: int = 0):
     mask = synth.vd_poisson_mask(dims, 8.0, 20, 0)
     pts = synth.mask_points(mask)
     N = len(pts)
-    vol = synth.random_ellipses((NX, NY, NZ), 20, rng)
+    vol = synth.random_ellipses((NX, NY, NZ), 20, rng, planes=(lo_s, hi_s))  # this rank's slab only
     maps3 = synth.coil_maps_cylinder((NX, NY, NZ), C, rng, xp=torch, device=dev)  # (C, NX*NY*NZ)
     # this rank's slices: maps (nloc, C, D), acquisition through the 3-D Cartesian model
     maps = maps3.view(C, NX, D)[:, lo_s:hi_s].permute(1, 0, 2).contiguous()
     del maps3
-    x_true = torch.from_numpy(vol.reshape(NX, D)[lo_s:hi_s].astype(np.complex64)).to(dev)
+    x_true = torch.from_numpy(vol.reshape(nloc, D).astype(np.complex64)).to(dev)
     kern = CartesianKernel(dims, [cartesian_plan(dims, pts)], batch=nloc)
     y2 = kern.forward(maps, x_true)  # (nloc, C, N) per-slice data
     sig = 0.01 * float(torch.abs(y2).max())
@@ -188,17 +191,17 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256, pool: int = 0):
     # the pipeline runs twice; the first run (library handles, graph capture, allocator) is a warm-up
     for _rep in range(2):
         torch.cuda.synchronize()
-        t_start = time.perf_counter()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record()
         y = dec(kx.contiguous()) if dec is not None else y2
-        torch.cuda.synchronize()
-        t_dec = time.perf_counter()
+        ev[1].record()
         maps0, y0, comp = compress_slices(maps, y, C)
-        torch.cuda.synchronize()
-        t_comp = time.perf_counter()
-        t_solve0 = time.perf_counter()
+        ev[2].record()
         res = cs.coil_sketching_recon_batched(kern, maps0, y0, cfg, dims)
+        ev[3].record()
         torch.cuda.synchronize()
-        t_end = time.perf_counter()
+        t_start, t_dec, t_comp, t_end = 0.0, *(ev[0].elapsed_time(e) / 1e3 for e in ev[1:])
+        t_solve0 = t_comp
     if os.environ.get("SR_PROFILE_RECON") and rank == 0:
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -254,9 +257,7 @@ def run_cfg2(with_oracle: bool, nslices_total: int = 256, pool: int = 0):
             line["cpu_pool"] = {"slices": k, "processes": min(cores, k), "cores": cores, "wall_s": t_pool,
                                 "extrapolated_s": t_pool * nslices_total / k,
                                 "nrmse_max": max(_nrmse(xs[sl], outs[sl]) for sl in range(k))}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    return full
+    return line
 
 
 def _lib_supported(n):
@@ -321,12 +322,14 @@ def run_cfg4(with_oracle: bool, scale: float = 1.0, outer: int = 10, inner: int 
     out = torch.empty_like(xin)
     eng._normal(smaps, xin, out)
     torch.cuda.synchronize()
-    reps = 3
-    t0 = time.perf_counter()
+    reps = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     for _ in range(reps):
         eng._normal(smaps, xin, out)
+    e1.record()
     torch.cuda.synchronize()
-    t_apply = _max_over_ranks((time.perf_counter() - t0) / reps, world, dev)
+    t_apply = _max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps, world, dev)
     if os.environ.get("SR_PROFILE_APPLY") and rank == 0:
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
@@ -339,15 +342,21 @@ def run_cfg4(with_oracle: bool, scale: float = 1.0, outer: int = 10, inner: int 
             eng.run(2, inner)
             torch.cuda.synchronize()
         print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25), flush=True)
-    t0 = time.perf_counter()
-    res = eng.run(outer, inner)
-    torch.cuda.synchronize()
-    t_recon = _max_over_ranks(time.perf_counter() - t0, world, dev)
+    if outer > 0:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = eng.run(outer, inner)
+        e1.record()
+        torch.cuda.synchronize()
+        t_recon = _max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)
+    else:
+        res, t_recon = None, None
     line = {"config": 4, "what": f"3-D cones {dims}, N={N}, KB 1.25x/w4, C={C} -> {V}+{S}, "
                                  f"{outer}x{inner} FISTA, coils sharded over {world} GPU(s)",
             "n_gpus": world, "scaling": "strong", "sketched_normal_apply_s": t_apply,
-            "recon_wall_s": t_recon, "plan_build_s": t_plan, "objectives": res.objectives[:, 0].tolist(),
-            "counts": res.counts, "data": "synthetic"}
+            "recon_wall_s": t_recon, "plan_build_s": t_plan,
+            "objectives": None if res is None else res.objectives[:, 0].tolist(),
+            "counts": None if res is None else res.counts, "data": "synthetic"}
     if with_oracle and rank == 0:
         # full-size CPU reference path on a bounded sample: the sketched normal op of ONE of the
         # 16 sketched coils through the oracle (numpy complex128, one core, tap tables per chunk of
@@ -376,8 +385,7 @@ def run_cfg4(with_oracle: bool, scale: float = 1.0, outer: int = 10, inner: int 
                                      "numpy complex128, one core, interpolator construction excluded, x 16")
         line["cpu_cores"] = 1
         line["speedup_apply_vs_cpu"] = line["cpu_oracle_apply_extrapolated_s"] / t_apply
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    return line if rank == 0 else None
 
 
 def main():
@@ -393,11 +401,13 @@ def main():
     ap.add_argument("--inner", type=int, default=10)
     a = ap.parse_args()
     if a.config in (0, 3):
-        run_2d(a.config, a.oracle)
+        line = run_2d(a.config, a.oracle)
     elif a.config == 2:
-        run_cfg2(a.oracle, a.slices, a.oracle_pool)
+        line = run_cfg2(a.oracle, a.slices, a.oracle_pool)
     else:
-        run_cfg4(a.oracle, a.scale, a.outer, a.inner)
+        line = run_cfg4(a.oracle, a.scale, a.outer, a.inner)
+    if line is not None:
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
