@@ -231,6 +231,17 @@ int sr_lincomb(sr_c64* out, const sr_c64* X, const sr_c64* Y, const sr_c64* Z,
 /* K7 -- per-slice scalar bookkeeping on the device:
  * op 0 power iteration step (linops.py:776-781), op 1 CG alpha, op 2 CG beta
  * (solvers.py:218-228). */
+/* K7 fused CG vector step of _cg_loop (solvers.py:206-229) for `batch` slices after the matvec
+ * mp = M p: alpha = rs / <p, mp>, x += alpha p, r -= alpha mp, rs_new = |r|^2, p = r + beta p,
+ * in three launches with fixed-order reductions (bit-reproducible).  pdot, prs: (batch,
+ * sr_reduce_nparts()) double2 scratch; state (batch, 4) doubles [rs0, rs1, active, iterations]
+ * set by the caller before the first step (rs0 = |r0|^2, active = 1, iterations = 0);
+ * parity = iteration & 1.  A slice stops updating (the reference's break) when sqrt(rs) <=
+ * tol_abs or <p, mp> <= 0; `iterations` then equals the reference's iteration count.  hist:
+ * NULL or (batch, hist_len + 1) doubles, hist[b][it] = sqrt(rs) after iteration it. */
+int sr_cg_step(sr_c64* x, sr_c64* r, sr_c64* p, const sr_c64* mp, double* pdot, double* prs, double* state,
+               double* hist, int hist_len, long long n, long long bstride, int batch, int parity,
+               double tol_abs, void* stream);
 int sr_scalar_op(int op, const double* in0, const double* in1, double* state, float* coefA,
                  float* coefB, int* flags, int batch, void* stream);
 

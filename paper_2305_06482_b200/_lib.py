@@ -67,6 +67,7 @@ SIGNATURES = {
     "sr_nufft_adjoint": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                          _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_partial_blocks": [_ll],
+    "sr_cg_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _ll, _ll, _i, _i, C.c_double, _vp],
     "sr_cart3_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sr_cart3_forward": [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _ll, _vp, _vp, _vp, _vp],
     "sr_cart3_adjoint": [_vp, _ll, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _vp],

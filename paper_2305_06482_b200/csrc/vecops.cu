@@ -132,11 +132,132 @@ __global__ void k_scalar(int op, const double2* __restrict__ in0, const double2*
   }
 }
 
+// ---------------------------------------------------------------- fused CG (K7)
+// One conjugate-gradient iteration of _cg_loop (solvers.py:206-229) for B independent slices,
+// after the matvec mp = M p, in three launches (k_reduce_partial <p, mp>, k_cg_xr, k_cg_p)
+// instead of two reductions, two scalar kernels and three linear combinations.  Per-slice
+// state (double): [rs(0), rs(1), active, iterations]; rs ping-pongs on the iteration parity
+// so no block overwrites a value another block of the same launch still reads.  Every block
+// of a slice reduces the slice's partials itself in the same fixed order, so the decisions and
+// coefficients are identical in all blocks and the results are bit-reproducible.
+__device__ __forceinline__ double2 sum_parts(const double2* __restrict__ part, int nparts) {
+  __shared__ double2 s_sum;
+  if (threadIdx.x == 0) {
+    double sr = 0.0, si = 0.0;
+    for (int k = 0; k < nparts; ++k) {
+      sr += part[k].x;
+      si += part[k].y;
+    }
+    s_sum = make_double2(sr, si);
+  }
+  __syncthreads();
+  return s_sum;
+}
+
+// alpha = rs / <p, mp> (if active, <p, mp> > 0 and sqrt(rs) > tol); x += alpha p; r -= alpha mp;
+// per-block partials of |r|^2
+__global__ void __launch_bounds__(RED_THREADS)
+k_cg_xr(float2* __restrict__ x, float2* __restrict__ r, const float2* __restrict__ p,
+        const float2* __restrict__ mp, const double2* __restrict__ pdot, double* __restrict__ state,
+        double2* __restrict__ prs, long long n, long long bstride, int parity, double tol_abs) {
+  const int b = blockIdx.y;
+  double* stb = state + 4 * (long long)b;
+  const double2 dn = sum_parts(pdot + (long long)b * gridDim.x, gridDim.x);
+  const double rs = stb[parity];
+  const bool go = stb[2] != 0.0 && sqrt(rs) > tol_abs;
+  const bool upd = go && dn.x > 0.0;
+  const float alpha = upd ? (float)(rs / dn.x) : 0.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (go) stb[3] += 1.0;       // iterations entered (a denominator break still counts, as in the reference)
+    if (!upd) stb[2] = 0.0;      // the reference breaks: this slice keeps x and r from here on
+  }
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  const long long o = b * bstride;
+  double sr = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    float2 rv = r[o + i];
+    if (upd) {
+      const float2 pv = p[o + i], mv = mp[o + i];
+      float2 xv = x[o + i];
+      xv.x = fmaf(alpha, pv.x, xv.x);
+      xv.y = fmaf(alpha, pv.y, xv.y);
+      x[o + i] = xv;
+      rv.x = fmaf(-alpha, mv.x, rv.x);
+      rv.y = fmaf(-alpha, mv.y, rv.y);
+      r[o + i] = rv;
+    }
+    sr += (double)rv.x * rv.x + (double)rv.y * rv.y;
+  }
+  __shared__ double rr[RED_THREADS];
+  rr[threadIdx.x] = sr;
+  __syncthreads();
+  for (int s = RED_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) rr[threadIdx.x] += rr[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) prs[(long long)b * gridDim.x + blockIdx.x] = make_double2(rr[0], 0.0);
+}
+
+// rs_new = |r|^2; beta = rs_new / rs; p = r + beta p (active slices); rs -> the other parity slot;
+// hist[it] = sqrt(rs_new) if hist is given (the residual history of _cg_loop)
+__global__ void __launch_bounds__(RED_THREADS)
+k_cg_p(float2* __restrict__ p, const float2* __restrict__ r, const double2* __restrict__ prs,
+       double* __restrict__ state, double* __restrict__ hist, int hist_len, long long n, long long bstride,
+       int parity) {
+  const int b = blockIdx.y;
+  double* stb = state + 4 * (long long)b;
+  const double rs_new = sum_parts(prs + (long long)b * gridDim.x, gridDim.x).x;
+  const double rs = stb[parity];
+  const bool act = stb[2] != 0.0;
+  const float beta = (act && rs != 0.0) ? (float)(rs_new / rs) : 0.f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    stb[parity ^ 1] = act ? rs_new : rs;
+    if (act && hist) {
+      const int it = (int)stb[3];
+      if (it >= 1 && it <= hist_len) hist[(long long)b * (hist_len + 1) + it] = sqrt(rs_new);
+    }
+  }
+  if (!act) return;
+  const long long chunk = (n + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  const long long o = b * bstride;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float2 rv = r[o + i];
+    float2 pv = p[o + i];
+    pv.x = fmaf(beta, pv.x, rv.x);
+    pv.y = fmaf(beta, pv.y, rv.y);
+    p[o + i] = pv;
+  }
+}
+
 }  // namespace
 
 extern "C" {
 
 int sr_reduce_nparts(void) { return RED_BLOCKS; }
+
+// Fused CG vector step (see k_cg_xr / k_cg_p): after mp = M p.  pdot, prs: (batch, RED_BLOCKS)
+// double2 scratch; state: (batch, 4) double [rs0, rs1, active, iterations] initialised by the
+// caller (rs0 = |r0|^2, active = 1, iterations = 0); parity = iteration index & 1; hist: NULL or
+// (batch, hist_len + 1) doubles receiving sqrt(rs) after iteration it at [it].
+int sr_cg_step(sr_c64* x, sr_c64* r, sr_c64* p, const sr_c64* mp, double* pdot, double* prs, double* state,
+               double* hist, int hist_len, long long n, long long bstride, int batch, int parity,
+               double tol_abs, void* stream) {
+  if (n < 0 || batch < 1 || !x || !r || !p || !mp || !pdot || !prs || !state || (parity & ~1)) return SR_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid(RED_BLOCKS, batch);
+  k_reduce_partial<<<grid, RED_THREADS, 0, st>>>(RED_DOT, (const float2*)p, (const float2*)mp, n, bstride,
+                                                 (double2*)pdot);
+  SR_CHECK_LAUNCH();
+  k_cg_xr<<<grid, RED_THREADS, 0, st>>>((float2*)x, (float2*)r, (const float2*)p, (const float2*)mp,
+                                        (const double2*)pdot, state, (double2*)prs, n, bstride, parity, tol_abs);
+  SR_CHECK_LAUNCH();
+  k_cg_p<<<grid, RED_THREADS, 0, st>>>((float2*)p, (const float2*)r, (const double2*)prs, state, hist, hist_len,
+                                       n, bstride, parity);
+  SR_CHECK_LAUNCH();
+  return SR_OK;
+}
 
 // partial: (batch, RED_BLOCKS) double2 workspace; result: (batch,) double2
 int sr_reduce(int mode, const sr_c64* a, const sr_c64* b, long long n, long long bstride,

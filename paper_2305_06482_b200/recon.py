@@ -276,33 +276,28 @@ class SketchedReconEngine:
     def _cg_solve(self, smaps, sol, rhs, shift_coef, iters: int):
         """sol = `iters` CG steps on (A_s^H A_s + shift I) sol = rhs from sol = 0 (_cg_loop,
         solvers.py:206-229); shift_coef (B, 4) = {1, shift, 0, 0} is the K1 epilogue of the matvec.
-        A slice whose residual vanishes or whose curvature p^H M p <= 0 stops updating, as the
-        reference's loop breaks (state kept on the device, no host sync)."""
+        Per iteration: K1 with the shift epilogue, then the fused vector step (csrc/vecops.cu
+        sr_cg_step: <p, Mp>, x/r update with |r|^2, p update; fixed-order reductions).  A slice
+        whose residual vanishes or whose curvature p^H M p <= 0 stops updating, as the reference's
+        loop breaks (state kept on the device, no host sync)."""
         B, D, st = self.B, self.D, dv.stream()
         sol.zero_()
         r = rhs.clone()
         p = r.clone()
         mp = torch.empty_like(r)
         nparts = _lib.lib().sr_reduce_nparts()
-        part = torch.empty(B, nparts, 2, dtype=torch.float64, device=self.dev)
+        pdot = torch.empty(B, nparts, 2, dtype=torch.float64, device=self.dev)
+        prs = torch.empty_like(pdot)
         rs = torch.empty(B, 2, dtype=torch.float64, device=self.dev)
-        den = torch.empty_like(rs)
-        state = torch.zeros(B, 2, dtype=torch.float64, device=self.dev)
-        cA = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
-        cB = torch.zeros_like(cA)
-        _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
+        state = torch.zeros(B, 4, dtype=torch.float64, device=self.dev)
+        _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(pdot), dv.ptr(rs), st)
         state[:, 0] = rs[:, 0]
-        state[:, 1] = (rs[:, 0] > 0).to(torch.float64)  # sqrt(rs) <= 0 stops at once
-        for _ in range(iters):
+        state[:, 2] = 1.0
+        for it in range(iters):
             self.counter.add("coil_transform", 2 * self.chat)
             self._normal(smaps, p, mp, coef=shift_coef, u=p)
-            _lib.call("sr_reduce", 1, dv.ptr(p), dv.ptr(mp), D, D, B, dv.ptr(part), dv.ptr(den), st)
-            _lib.call("sr_scalar_op", 1, None, dv.ptr(den), dv.ptr(state), dv.ptr(cA), dv.ptr(cB), None, B, st)
-            _lib.call("sr_lincomb", dv.ptr(sol), dv.ptr(sol), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
-            _lib.call("sr_lincomb", dv.ptr(r), dv.ptr(r), dv.ptr(mp), None, dv.ptr(cB), 0, 0, 0, D, D, B, st)
-            _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(part), dv.ptr(rs), st)
-            _lib.call("sr_scalar_op", 2, dv.ptr(rs), None, dv.ptr(state), dv.ptr(cA), None, None, B, st)
-            _lib.call("sr_lincomb", dv.ptr(p), dv.ptr(r), dv.ptr(p), None, dv.ptr(cA), 0, 0, 0, D, D, B, st)
+            _lib.call("sr_cg_step", dv.ptr(sol), dv.ptr(r), dv.ptr(p), dv.ptr(mp), dv.ptr(pdot), dv.ptr(prs),
+                      dv.ptr(state), None, 0, D, D, B, it & 1, 0.0, st)
         return sol
 
     def _cg(self, smaps, inner: int):

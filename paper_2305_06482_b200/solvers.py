@@ -229,30 +229,57 @@ def _coil_count(a) -> int:
 
 
 def _cg_loop(matvec, b, x0, max_iters, tol_abs, history=None):
-    """Plain CG on M x = b (solvers.py:206-229); device tensors, fixed-order dots."""
-    x = dv.c64(x0).clone()
-    b = dv.c64(b)
-    r = b - matvec(x) if bool(torch.any(x != 0)) else b.clone()
+    """Plain CG on M x = b (solvers.py:206-229) on the device: per iteration the caller's matvec
+    and the fused vector step of csrc/vecops.cu (sr_cg_step: alpha, x/r update, |r|^2, beta,
+    p update, fixed-order reductions).  The reference's breaks (sqrt(rs) <= tol_abs before an
+    iteration, p^H M p <= 0 inside it) freeze the device state instead of returning early, so the
+    loop never reads a scalar back; the iteration count and the residual history are read once
+    at the end."""
+    x = dv.c64(x0).clone().view(1, -1)
+    b = dv.c64(b).view(1, -1)
+    D = x.shape[1]
+    r = (b - matvec(x[0]).view(1, -1)) if bool(torch.any(x != 0)) else b.clone()
     p = r.clone()
-    rs = float(dev_norm2(r.view(1, -1))[0])
-    res = [math.sqrt(rs)]
-    it = 0
-    for it in range(1, max_iters + 1):
-        if math.sqrt(rs) <= tol_abs:
-            it -= 1
-            break
-        mp = matvec(p)
-        denom = float(dev_vdot(p.view(1, -1), mp.view(1, -1))[0, 0])
-        if denom <= 0:
-            break
-        alpha = rs / denom
-        lincomb(x, x, p, cx=1.0, cy=alpha)
-        lincomb(r, r, mp, cx=1.0, cy=-alpha)
-        rs_new = float(dev_norm2(r.view(1, -1))[0])
-        res.append(math.sqrt(rs_new))
-        lincomb(p, r, p, cx=1.0, cy=rs_new / rs)
-        rs = rs_new
-    return x, it, np.array(res)
+    st = dv.stream()
+    nparts = _lib.lib().sr_reduce_nparts()
+    pdot = torch.empty(1, nparts, 2, dtype=torch.float64, device=x.device)
+    prs = torch.empty_like(pdot)
+    rs0 = torch.empty(1, 2, dtype=torch.float64, device=x.device)
+    _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, 1, dv.ptr(pdot), dv.ptr(rs0), st)
+    state = torch.zeros(1, 4, dtype=torch.float64, device=x.device)
+    state[:, 0] = rs0[:, 0]
+    state[:, 2] = 1.0
+    hist = torch.full((1, max_iters + 1), float("nan"), dtype=torch.float64, device=x.device)
+    hist[:, 0] = torch.sqrt(rs0[:, 0])
+    for it in range(max_iters):
+        mp = matvec(p[0]).view(1, -1).contiguous()
+        _lib.call("sr_cg_step", dv.ptr(x), dv.ptr(r), dv.ptr(p), dv.ptr(mp), dv.ptr(pdot), dv.ptr(prs),
+                  dv.ptr(state), dv.ptr(hist), max_iters, D, D, 1, it & 1, float(tol_abs), st)
+    iters = int(state[0, 3].item())
+    # one history entry per completed update (a p^H M p <= 0 break counts the iteration but
+    # appends nothing); entries never written stay NaN
+    h = hist[0].cpu().numpy()
+    return x[0], iters, h[~np.isnan(h)]
+
+
+def _shifted_normal(a: LinOp, shift: float):
+    """v -> A^H A v + shift v; for a SenseOperator one fused K1 call with the epilogue
+    {1, shift} (no separate vector op), counting 2C coil transforms like adjoint(forward)."""
+    if isinstance(a, SenseOperator):
+        coef = torch.tensor([[1.0, float(shift), 0.0, 0.0]], dtype=torch.float32, device=a.maps_dev.device)
+
+        def mv(v):
+            vv = v.view(1, -1).contiguous()
+            out = torch.empty_like(vv)
+            a.normal_into(vv, out, coef=coef, u=vv)
+            return out[0]
+        return mv
+    nop = _NormalOp(a)
+
+    def mv(v):
+        out = nop._forward(v)
+        return out + shift * v if shift else out
+    return mv
 
 
 def cg_normal(a: LinOp, y, lam: float, x0: Image, cfg: SolverConfig) -> SolveResult:
@@ -263,10 +290,7 @@ def cg_normal(a: LinOp, y, lam: float, x0: Image, cfg: SolverConfig) -> SolveRes
     n0 = _coil_count(a)
     b = a._adjoint(dv.c64(y))
     tol_abs = cfg.tol * math.sqrt(float(dev_norm2(b.view(1, -1))[0]))
-    nop = _NormalOp(a)
-
-    def matvec(v):
-        return nop._forward(v) + lam * v
+    matvec = _shifted_normal(a, lam)
 
     x, iters, res = _cg_loop(matvec, b, x0.values, cfg.max_iters, tol_abs)
     return SolveResult(Image(x0.shape, x), iters, res if cfg.record_history else np.empty(0),
@@ -286,8 +310,9 @@ def fista(grad, prox, L: float, x0: Image, cfg: SolverConfig, objective=None,
     t_k = 1.0
     hist = []
     iters = 0
+    v = torch.empty_like(x)
     for iters in range(1, cfg.max_iters + 1):
-        v = z - step * grad(z)
+        lincomb(v, z, grad(z), cx=1.0, cy=-step)
         x_new = prox(v, step)
         t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_k * t_k))
         z = torch.empty_like(x_new)
@@ -323,12 +348,21 @@ def reconstruct(a: SenseOperator, y, reg: Regularizer, cfg: SolverConfig, x0: Im
         if lipschitz is None:
             lipschitz = normal_max_eig(a) / cfg.step_scale
         yt = dv.c64(y)
-        nop = _NormalOp(a)
         with a.paused_counts():
-            aty = a._adjoint(yt)  # A^H y once; each grad() still tallies 2C like the reference
+            aty = a._adjoint(yt).view(1, -1)  # A^H y once; each grad() still tallies 2C like the reference
+        if isinstance(a, SenseOperator):
+            gcoef = torch.tensor([[1.0, 0.0, -1.0, 0.0]], dtype=torch.float32, device=aty.device)
 
-        def grad(v):
-            return nop._forward(v) - aty
+            def grad(v):  # A^H A v - A^H y in one fused K1 call (epilogue {1, 0, -1})
+                vv = v.view(1, -1).contiguous()
+                out = torch.empty_like(vv)
+                a.normal_into(vv, out, coef=gcoef, d=aty)
+                return out[0]
+        else:
+            nop = _NormalOp(a)
+
+            def grad(v):
+                return nop._forward(v) - aty[0]
 
         def prox(v, step):
             return reg.prox(v, step)
@@ -424,13 +458,8 @@ def _pdhg_tv(a: SenseOperator, y, reg: Regularizer, x0: Image, cfg: SolverConfig
     p = torch.zeros(1, nd * D, dtype=torch.complex64, device=x.device)
     sig_t = torch.full((1,), sigma, dtype=torch.float32, device=x.device)
     tau_t = torch.full((1,), tau, dtype=torch.float32, device=x.device)
-    nop = _NormalOp(a)
     st = dv.stream()
-
-    def matvec(u):
-        out = nop._forward(u)
-        lincomb(out, out, u, cx=1.0, cy=1.0 / tau)
-        return out
+    matvec = _shifted_normal(a, 1.0 / tau)  # one fused K1 call per CG matvec
 
     hist = []
     iters = 0
