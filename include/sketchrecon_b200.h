@@ -190,6 +190,13 @@ int sr_wavelet_ana2_nblocks(int h, int w);
  * (solvers.py:292-293). coef and out must differ. */
 int sr_wavelet_syn2(const sr_c64* coef, sr_c64* out, int h, int w, int ld, long long bs,
                     int batch, sr_c64* zout, const sr_c64* xold, float beta, void* stream);
+/* K6 -- the whole 2-D L1-wavelet prox (solvers.py:71-81, linops.py:654-702) in one call: `levels`
+ * thresholded analysis levels into the scratch pair buf0/buf1 (each ny x nx per slice, row
+ * stride nx, slice stride bs) and the synthesis into out, with the optional FISTA momentum
+ * epilogue zout = out + beta (out - xold) on level 0 (out may alias xold, not v). */
+int sr_wavelet_prox2(const sr_c64* v, sr_c64* out, sr_c64* buf0, sr_c64* buf1, int ny, int nx, long long bs,
+                     int batch, int levels, const float* thresh, float hthresh, sr_c64* zout, const sr_c64* xold,
+                     float beta, void* stream);
 int sr_wavelet_levels_max(void);
 /* K6 n-D -- one axis of one DB4 level (analysis or synthesis) over the (h0, h1, h2)
  * corner of (n0, n1, n2) arrays, for 1-D and 3-D grids (linops.py:619-651, 677-702);

@@ -39,6 +39,7 @@ SIGNATURES = {
     "sr_wavelet_ana2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _f, _i, _vp, _vp],
     "sr_wavelet_ana2_nblocks": [_i, _i],
     "sr_wavelet_syn2": [_vp, _vp, _i, _i, _i, _ll, _i, _vp, _vp, _f, _vp],
+    "sr_wavelet_prox2": [_vp, _vp, _vp, _vp, _i, _i, _ll, _i, _i, _vp, _f, _vp, _vp, _f, _vp],
     "sr_wavelet_levels_max": [],
     "sr_wavelet_axis": [_vp, _vp, _i, _i, _i, _i, _i, _ll, _i, _i, _i, _vp, _f, _i, _i, _vp, _vp, _vp, _f, _vp],
     "sr_wavelet_axis_nblocks": [],

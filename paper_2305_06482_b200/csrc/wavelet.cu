@@ -229,4 +229,30 @@ int sr_wavelet_syn2(const sr_c64* coef, sr_c64* out, int h, int w, int ld, long 
   return SR_OK;
 }
 
+// The whole 2-D prox of Regularizer.prox (solvers.py:71-81) in one call: `levels` analysis levels
+// (v -> buf0/buf1 ping-pong, soft threshold on every detail band and on the last low-pass corner)
+// and the synthesis back into out with the FISTA momentum epilogue zout = out + beta (out - xold)
+// on level 0 -- the launches of WaveletEngine.prox issued from C (one host call per prox).
+int sr_wavelet_prox2(const sr_c64* v, sr_c64* out, sr_c64* buf0, sr_c64* buf1, int ny, int nx, long long bs,
+                     int batch, int levels, const float* thresh, float hthresh, sr_c64* zout, const sr_c64* xold,
+                     float beta, void* stream) {
+  if (levels < 1 || levels > 8 || !v || !out || !buf0 || !buf1) return SR_EINVAL;
+  sr_c64* bufs[2] = {buf0, buf1};
+  const sr_c64* src = v;
+  for (int l = 0; l < levels; ++l) {
+    const int rc = sr_wavelet_ana2(src, bufs[l % 2], ny >> l, nx >> l, nx, bs, batch, thresh, hthresh,
+                                   l == levels - 1, nullptr, stream);
+    if (rc) return rc;
+    src = bufs[l % 2];
+  }
+  for (int l = levels - 1; l >= 0; --l) {
+    sr_c64* dst = (l == 0) ? out : bufs[(l - 1) % 2];
+    const int rc = (l == 0) ? sr_wavelet_syn2(bufs[0], dst, ny, nx, nx, bs, batch, zout, xold, beta, stream)
+                            : sr_wavelet_syn2(bufs[l % 2], dst, ny >> l, nx >> l, nx, bs, batch, nullptr, nullptr,
+                                              0.f, stream);
+    if (rc) return rc;
+  }
+  return SR_OK;
+}
+
 }  // extern "C"

@@ -120,6 +120,11 @@ class WaveletEngine:
         thresh: device (B,) float32 thresholds or None with host `hthresh`.
         v must not alias out, self.buf.  out may alias xold.
         """
+        if not self.generic:  # 2-D: every level's launches from one C call (sr_wavelet_prox2)
+            _lib.call("sr_wavelet_prox2", dv.ptr(v), dv.ptr(out), dv.ptr(self.buf[0]), dv.ptr(self.buf[1]),
+                      self.ny, self.nx, self.D, self.batch, self.levels, dv.ptr(thresh), float(hthresh),
+                      dv.ptr(zout), dv.ptr(xold), float(beta), dv.stream())
+            return out
         src = v
         for l in range(self.levels):
             dst = self.buf[l % 2]

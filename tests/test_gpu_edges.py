@@ -199,10 +199,12 @@ def test_fused_sample_io_matches_separate_passes(cuda, dims, C):
     np.testing.assert_allclose(outs[True][2], outs[False][2], rtol=1e-7)
 
 
-@pytest.mark.parametrize("S,N,C", [(4, 5119, 32), (3, 700, 12), (2, 40, 40 // 2), (1, 33, 32)])
+@pytest.mark.parametrize("S,N,C", [(4, 5119, 32), (3, 700, 12), (2, 40, 40 // 2), (1, 33, 32),
+                                   (1, 16384, 16), (1, 81920, 16), (1, 5000, 32)])
 def test_tsqr_r_matches_lapack(cuda, S, N, C):
     """Batched tall-skinny Householder R (csrc/tsqr.cu) equals LAPACK's zgeqrf R (numpy.linalg.qr,
-    mode 'r') including the signs of its real diagonal; a zero column takes the tau = 0 path."""
+    mode "r") including the signs of its real diagonal; a zero column takes the tau = 0 path.  Single
+    large blocks take the many-CTA kernel (grid barriers)."""
     from paper_2305_06482_b200 import _device as dv
     from paper_2305_06482_b200 import _lib
     rng = np.random.default_rng(S * N + C)
