@@ -375,25 +375,40 @@ class SketchedReconEngine:
         if tol > 0.0 and (B != 1 or self.solver == "cg"):
             raise ValueError("inner-solver early stopping (tol > 0) runs FISTA / PDHG one slice at a time")
         t_start = time.perf_counter()
+        ev_start = torch.cuda.Event(enable_timing=True)
+        ev_start.record()
         if x0 is not None:
             self.x.copy_(x0)
         else:
             self.x.zero_()
-        obj0 = self.objective(self.x).cpu().numpy()
-        alive = np.ones(B, dtype=bool)
-        diverged = np.zeros(B, dtype=bool)
-        outer_run = np.zeros(B, dtype=np.int64)
+        # With a fixed inner count (tol = 0) nothing inside the loop needs a host decision: the
+        # sketch draws are made up front (host RNG, bit-identical, one upload), the divergence
+        # test, the frozen copy of a diverged slice, the objectives and the distances stay on the
+        # device, and everything is read back once at the end (CUDA events time the outers).
+        # A slice that diverges keeps its frozen image; the outers after the last live one are
+        # trimmed from the records and their coil transforms removed from the counter, so the
+        # report equals the reference's early exit (coil_sketch.py:300-302).  tol > 0 needs a
+        # host read per inner iteration anyway and keeps the per-outer checks on the host.
+        deferred = tol == 0.0
+        obj0_d = self.objective(self.x)
+        alive_d = torch.ones(B, dtype=torch.bool, device=self.dev)
+        outer_run_d = torch.zeros(B, dtype=torch.int64, device=self.dev)
         frozen = self.x.clone()
-        objs, cnts, walls, dists = [], [], [], []
+        obj_hist = torch.full((outer, B), float("inf"), dtype=torch.float64, device=self.dev)
+        dist_hist = torch.full((outer, B), float("nan"), dtype=torch.float64, device=self.dev)
+        cnts, evs = [], []
         lip = None
         ref_norm = None
         if x_ref is not None:
-            ref_norm = torch.linalg.vector_norm(x_ref.to(torch.complex128), dim=1).cpu().numpy()
+            ref_norm = torch.linalg.vector_norm(x_ref.to(torch.complex128), dim=1)
+        mats = [gen_sketch_matrix(self.sketch.with_seed(child_seed(self.sketch.seed, t)), self.C0).mat
+                for t in range(1, outer + 1)]
+        mats_d = torch.from_numpy(np.ascontiguousarray(np.stack(mats), dtype=np.float32)).to(self.dev)
+        self.chat = mats[0].shape[0]
+        t_done = 0
         for t in range(1, outer + 1):
             self.true_gradient(self.d)
-            sk = gen_sketch_matrix(self.sketch.with_seed(child_seed(self.sketch.seed, t)), self.C0)
-            self.chat = sk.mat.shape[0]
-            smaps = self._sketch(sk.mat)
+            smaps = self._sketch(mats_d[t - 1])
             if self.solver == "fista" and (lip is None or not reuse_step_size):
                 lam_max = self.power_lambda(smaps)
                 lip = lam_max / self.step_scale
@@ -418,33 +433,41 @@ class SketchedReconEngine:
                 self._pdhg(smaps, inner, tol)
             else:
                 self._cg(smaps, inner)
-            finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1).cpu().numpy()
-            obj = self.objective(self.x).cpu().numpy()
-            obj = np.where(finite, obj, np.inf)
-            objs.append(obj)
+            finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1)
+            obj = torch.where(finite, self.objective(self.x), torch.full_like(obj0_d, float("inf")))
+            obj_hist[t - 1] = obj
             cnts.append(self.counter.value("coil_transform"))
-            walls.append(time.perf_counter() - t_start)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            evs.append(ev)
             if x_ref is not None:
-                dd = torch.linalg.vector_norm((self.x - x_ref).to(torch.complex128), dim=1).cpu().numpy()
-                dists.append(dd / ref_norm)
-            else:
-                dists.append(np.full(B, np.nan))
-            newly = alive & ((~finite) | (obj > DIVERGENCE_FACTOR * obj0))
-            outer_run[alive] = t
-            if newly.any():
-                idx = torch.as_tensor(np.nonzero(newly)[0], device=self.dev)
-                frozen.index_copy_(0, idx, self.x.index_select(0, idx))
-                diverged |= newly
-                alive &= ~newly
-            if not alive.any():
+                dist_hist[t - 1] = torch.linalg.vector_norm((self.x - x_ref).to(torch.complex128), dim=1) / ref_norm
+            newly = alive_d & ((~finite) | (obj > DIVERGENCE_FACTOR * obj0_d))
+            outer_run_d = torch.where(alive_d, torch.full_like(outer_run_d, t), outer_run_d)
+            fr = torch.view_as_real(frozen)
+            fr.copy_(torch.where(newly.view(B, 1, 1), torch.view_as_real(self.x), fr))
+            alive_d = alive_d & ~newly
+            t_done = t
+            if not deferred and not bool(alive_d.any()):
                 break
+        # the one host read of the run
+        obj_h = obj_hist[:t_done].cpu().numpy()
+        outer_run = outer_run_d.cpu().numpy()
+        diverged = ~alive_d.cpu().numpy()
+        obj0 = obj0_d.cpu().numpy()
+        dists = list(dist_hist[:t_done].cpu().numpy())
+        walls = [ev_start.elapsed_time(e) / 1e3 for e in evs]
+        t_last = int(outer_run.max()) if B else t_done
+        if t_last < t_done:  # every slice stopped at t_last: drop the outers run past it
+            self.counter.add("coil_transform", cnts[t_last - 1] - cnts[t_done - 1])
+            obj_h, cnts, walls, dists = obj_h[:t_last], cnts[:t_last], walls[:t_last], dists[:t_last]
         x = self.x.clone()
         if diverged.any():
             idx = torch.as_tensor(np.nonzero(diverged)[0], device=self.dev)
             x.index_copy_(0, idx, frozen.index_select(0, idx))
         xr = torch.view_as_real(x)
         x = torch.view_as_complex(torch.where(torch.isfinite(xr), xr, torch.zeros_like(xr)).contiguous())
-        return EngineResult(x, np.array(objs), obj0, diverged, outer_run,
+        return EngineResult(x, obj_h, obj0, diverged, outer_run,
                             np.full(B, np.nan) if lip is None else lip.cpu().numpy(),
                             self.counter.asdict(), cnts, walls, dists)
 
