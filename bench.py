@@ -310,8 +310,12 @@ def run_extras(rank: int, world: int, dev) -> dict:
         out["recon"]["config2_wall_s"] = r2["gpu_wall_s"]
         out["sharded"]["config4"] = {k: r4[k] for k in ("what", "n_gpus", "scaling", "sketched_normal_apply_s",
                                                         "plan_build_s", "data")}
-        out["sharded"]["config4"]["collective"] = ("NCCL all-reduce (sum) of the 83.9 MB image-domain partial "
-                                                   "coil sum per apply" if world > 1 else "none (1 rank)")
+        if world > 1:
+            import torch.distributed as dist
+            out["sharded"]["config4"]["collective"] = (f"{dist.get_backend()} all-reduce (sum) of the 83.9 MB "
+                                                       "image-domain partial coil sum per apply")
+        else:
+            out["sharded"]["config4"]["collective"] = "none (1 rank)"
     return out if rank == 0 else {}
 
 
@@ -341,10 +345,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SR_DIST_BACKEND=gloo exercises the multi-rank logic on a box with fewer GPUs than ranks
+    # (ranks share devices round-robin; collectives through the host).  Timing runs use NCCL.
+    backend = os.environ.get("SR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 
     from paper_2305_06482_b200 import _lib
     _lib.lib()

@@ -38,10 +38,15 @@ def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SR_DIST_BACKEND=gloo exercises the multi-rank logic on a box with fewer GPUs than ranks
+    # (ranks share devices round-robin; collectives through the host).  Timing runs use NCCL.
+    backend = os.environ.get("SR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     return rank, world, dev
 
 
