@@ -87,6 +87,9 @@ int sr_cart_tune(int col_jc);
 /* Tuning: the coil-looped column pass prefetches the next coil's strip in registers (pf = 1,
  * 2 CTAs/SM, default) or not (pf = 0, 3 CTAs/SM). */
 int sr_cart_tune_colpf(int pf);
+/* Tuning: preferred L1 / shared-memory carveout (percent of the maximum shared memory, -1 =
+ * the driver's choice) of the three K1 passes; it bounds how many CTAs of a pass share an SM. */
+int sr_cart_tune_carveout(int pct);
 /* Tuning: the row FFT pass stores its output with TMA bulk copies (bulk = 1), through a
  * coalesced copy-out pass (0), or picks per size (2, default: bulk for 20-element groups with
  * Q >= 12, where it measured faster); rows shorter than min_n always use the copy-out. */

@@ -57,6 +57,7 @@ SIGNATURES = {
     "sr_group_select": [_i],
     "sr_cart_tune": [_i],
     "sr_cart_tune_colpf": [_i],
+    "sr_cart_tune_carveout": [_i],
     "sr_split_tune": [_i, _i],
     "sr_cart_tune_rows": [_i, _i],
     "sr_fused_config": [_i, _i, _i, _i],

@@ -7,6 +7,18 @@
 extern int sr_g_col_jc;  // coils per CTA of k_colnormal (0 = use k_colpass); cart.cu
 extern int sr_g_col_pf;  // k_colnormal: 1 = next coil's strip prefetched in registers (2 CTAs/SM), 0 = not (3 CTAs/SM)
 extern int sr_g_row_bulk, sr_g_row_bulk_min_n;  // rowfwd TMA bulk stores (on, min row length); cart.cu
+extern int sr_g_carveout;  // preferred shared-memory carveout (percent, -1 = driver default) of the column pass; cart.cu
+
+// apply the carveout knob to a kernel once per value (the L1 / shared split decides how many
+// CTAs of a pass fit an SM: the driver's default picked 135 KB for the column pass = 2 CTAs)
+template <typename K>
+inline int apply_carveout(K kern, int& applied) {
+  if (applied == sr_g_carveout) return SR_OK;
+  const int v = sr_g_carveout < 0 ? -1 : sr_g_carveout;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, v) != cudaSuccess) return SR_ECUDA;
+  applied = sr_g_carveout;
+  return SR_OK;
+}
 
 enum { COL_NORMAL = 0, COL_FWD = 1, COL_INV = 2, COL_FWD_G = 3, COL_INV_S = 4 };
 
@@ -531,6 +543,7 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
                   int batch, int ncoils, int ny, long long xbs, long long mbs, cudaStream_t st) {
   using R = RowCfg<P, Q>;
   static bool configured = false;
+  static int carve = -2;
   if (!configured) {
     if (cudaFuncSetAttribute(k_rowfwd<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)R::SMEM_FWD) != cudaSuccess)
@@ -550,6 +563,7 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
                   const float2* d, float oscale, cudaStream_t st) {
   using R = RowCfg<P, Q>;
   static bool configured = false;
+  static int carve = -2;
   if (!configured) {
     if (cudaFuncSetAttribute(k_rowinv<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)R::SMEM_INV) != cudaSuccess)
@@ -586,12 +600,14 @@ int launch_colnormal_t(float2* ws, const uint8_t* maskT, long long mbs, int batc
   using C = ColCfg<P, Q>;
   const size_t smem = sizeof(float2) * (2 * P * Q + C::CB * C::VSP);
   static bool configured = false;
+  static int carve = -2;
   if (!configured) {
     if (cudaFuncSetAttribute(k_colnormal<P, Q, NX, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return SR_ECUDA;
     configured = true;
   }
+  if (apply_carveout(k_colnormal<P, Q, NX, PF>, carve)) return SR_ECUDA;
   const int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
   dim3 grid(NX / C::CB, (ncoils + jc - 1) / jc, batch);
   k_colnormal<P, Q, NX, PF><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--group", default="", help="comma list of group sizes G for chunk -2")
     ap.add_argument("--stats", action="store_true", help="collect fused-kernel wait/item statistics")
     ap.add_argument("--colpf", default="", help="comma list of column-pass prefetch modes (1 / 0)")
+    ap.add_argument("--carveout", default="", help="comma list of shared-memory carveouts (percent, -1 = default); "
+                                                   "each runs the colpf list")
     ap.add_argument("--split", default="", help="semicolon list of jc,ja settings of the split-column schedule (chunk -3)")
     ap.add_argument("--multistream", default="", help="semicolon list of chunk,streams for the three-pass schedule")
     args = ap.parse_args()
@@ -35,10 +37,13 @@ def main():
     kern, smaps, x = w["kern"], w["smaps"], w["x"]
     out = torch.empty_like(x)
     from paper_2305_06482_b200 import _lib
-    for pf in [int(c) for c in args.colpf.split(",") if c]:
-        _lib.call("sr_cart_tune_colpf", pf)
-        t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=0), args.steps, 3, torch.cuda.synchronize)
-        print(json.dumps({"colpf": pf, "ms_per_apply": t * 1e3 / args.steps}), flush=True)
+    for cv in [int(c) for c in args.carveout.split(",") if c] or [None]:
+        if cv is not None:
+            _lib.call("sr_cart_tune_carveout", cv)
+        for pf in [int(c) for c in args.colpf.split(",") if c]:
+            _lib.call("sr_cart_tune_colpf", pf)
+            t = bench.time_applies(lambda: kern.normal(smaps, x, out, chunk=0), args.steps, 3, torch.cuda.synchronize)
+            print(json.dumps({"carveout": cv, "colpf": pf, "ms_per_apply": t * 1e3 / args.steps}), flush=True)
     _lib.call("sr_cart_tune_colpf", 1)
     for cfg in [c for c in args.split.split(";") if c]:
         jc, ja = (int(v) for v in cfg.split(","))
