@@ -195,7 +195,7 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
          const float2* __restrict__ u, const float2* __restrict__ d, float oscale) {
-  using S = RowShape<P, Q>;
+  using S = RowShapeNP<P, Q>;  // rows contiguous in shared memory: one bulk copy per row
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   extern __shared__ __align__(16) float2 dsm[];
   float2* t2 = dsm;
@@ -214,29 +214,43 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   const float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   const int nvalid = min(ROWS, ny - row0) * N;
+  // Coil tiles are double-buffered.  With even P (16-byte aligned rows, S::VEC) every row of the
+  // tile is one bulk-async copy global -> shared on the TMA unit (no register staging, no
+  // per-element LDGSTS), completing on the buffer's mbarrier; odd P keeps the 8-byte cp.async path.
+  __shared__ __align__(8) uint64_t tbar[2];
+  const int nrows = min(ROWS, ny - row0);
+  if constexpr (S::VEC) {
+    if (tid == 0) {
+      mbar_init(&tbar[0], 1);
+      mbar_init(&tbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   auto issue_tile = [&](int j) {
     const float2* wj = wb + j * D;
     float2* dst = bufs + (j & 1) * (ROWS * S::VS);
     if constexpr (S::VEC) {
-      for (int e = 2 * tid; e < nvalid; e += 2 * T) {
-        const int l3 = e / N, pos = e - l3 * N;
-        cp_async16(dst + l3 * S::VS + S::pad(pos), wj + e);
-      }
+      // the buffer was last read through the generic proxy (previous coil, behind a barrier)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (tid == 0) mbar_arrive_expect(&tbar[j & 1], (unsigned)(nrows * N * 8));
+      if (tid < nrows) bulk_g2s(dst + tid * S::VS, wj + (long long)tid * N, N * 8, &tbar[j & 1]);
     } else {
       for (int e = tid; e < nvalid; e += T) {
         const int l3 = e / N, pos = e - l3 * N;
         cp_async8(dst + l3 * S::VS + S::pad(pos), wj + e);
       }
+      cp_async_commit();
     }
-    cp_async_commit();
   };
   issue_tile(0);
   for (int j = 0; j < ncoils; ++j) {
-    if (j + 1 < ncoils) {
-      issue_tile(j + 1);
-      cp_async_wait<1>();
+    if (j + 1 < ncoils) issue_tile(j + 1);
+    if constexpr (S::VEC) {
+      mbar_wait(&tbar[j & 1], (j >> 1) & 1);
     } else {
-      cp_async_wait<0>();
+      if (j + 1 < ncoils) cp_async_wait<1>();
+      else cp_async_wait<0>();
     }
     __syncthreads();
     float2* buf = bufs + (j & 1) * (ROWS * S::VS);

@@ -100,6 +100,20 @@ struct RowShape {
   __device__ __forceinline__ static int pad(int pos) { return (P_ == 1) ? pos : pos + (GS - P_) * (pos / P_); }
 };
 
+// Row tiles without group padding (groups of P back to back, rows padded to VS = P (mod 16)):
+// a whole row is contiguous in shared memory, so one bulk-async copy moves it (k_rowinv).
+// With P = 20 the 128-bit group loads see 2-way bank conflicts, which the DRAM-bound row IFFT
+// pass absorbs.
+template <int P_, int Q_>
+struct RowShapeNP {
+  static constexpr int P = P_, Q = Q_, N = P_ * Q_;
+  static constexpr bool VEC = (P_ % 2 == 0) && (P_ > 1);
+  static constexpr int GS = P_;
+  static constexpr int VS0 = N;
+  static constexpr int VS = VS0 + ((((P_ % 16) - (VS0 % 16)) % 16 + 16) % 16);
+  __device__ __forceinline__ static int pad(int pos) { return pos; }
+};
+
 template <int P, bool VEC>
 __device__ __forceinline__ void lds_group(float2* g, const float2* gp) {
   if constexpr (VEC) {
