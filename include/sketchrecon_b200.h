@@ -54,32 +54,15 @@ int sr_fft_split(int n, int* P, int* Q);
  *   coef: NULL -> out = acc; else device float4 per slice {s_acc, s_u, s_d, -}:
  *         out = s_acc*acc + s_u*u + s_d*d  (FISTA: z - step*(acc + d); CG: acc + lam*v)
  *   chunk: 0 = three launches (row FFT, column FFT-mask-IFFT, row IFFT + coil sum)
- *          over the whole batch; > 0: the three launches per group of `chunk` slices;
- *          -1: one persistent launch with an L2-resident workspace ring (cart_fused.cu,
- *          sizes with sr_fused_normal_supported)
+ *          over the whole batch; > 0: the three launches per group of `chunk` slices
+ *          (the single-launch / L2-exchange schedules of round 1 were measured slower and
+ *          removed)
  *   ws: sr_cart_ws_bytes(batch, ncoils, ny, nx, chunk) bytes */
 int sr_cart_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps,
                    long long map_bstride, const uint8_t* maskT, long long mask_bstride,
                    sr_c64* out, sr_c64* ws, int batch, int ncoils, int ny, int nx,
                    const float* coef, const sr_c64* u, const sr_c64* d, int chunk,
                    void* stream);
-
-/* chunk == -2 (group schedule, cart_group.cu): one persistent launch in which groups of
- * G co-resident CTAs share each coil image through an L2-resident scratch image, so the
- * coil workspace never streams through HBM.  Instantiated for the (ny, nx) pairs below
- * report 1 from sr_group_normal_supported; sr_group_ngroups is the number of CTA groups
- * the current device runs concurrently (0 if unsupported). */
-int sr_group_normal_supported(int ny, int nx);
-int sr_group_ngroups(int ny, int nx);
-/* Tuning: prefer group size g where an instantiation exists (0 = each size's default). */
-int sr_group_select(int g);
-
-/* chunk == -3 (split-column schedule, cart_split.cu; square images of the instantiated sizes):
- * three launches whose middle pass is register-only -- the column FFT's DFT_Q step runs in the
- * row passes, which own the rows it combines.  sr_split_tune sets the middle pass's coils per
- * CTA (jc, default 4) and the number of coil ranges the first pass splits a slice into (ja,
- * default 2). */
-int sr_split_tune(int jc, int ja);
 
 /* Tuning of the three-launch schedule: coils per CTA of the column pass (0 = one coil per
  * CTA, the generic kernel; default 4). */
@@ -88,7 +71,8 @@ int sr_cart_tune(int col_jc);
  * 2 CTAs/SM, default) or not (pf = 0, 3 CTAs/SM). */
 int sr_cart_tune_colpf(int pf);
 /* Tuning: preferred L1 / shared-memory carveout (percent of the maximum shared memory, -1 =
- * the driver's choice) of the three K1 passes; it bounds how many CTAs of a pass share an SM. */
+ * the driver's choice, the measured best) of the K1 column pass; it bounds how many CTAs of
+ * the pass share an SM. */
 int sr_cart_tune_carveout(int pct);
 /* Tuning: the row FFT pass stores its output with TMA bulk copies (bulk = 1), through a
  * coalesced copy-out pass (0), or picks per size (2, default: bulk for 20-element groups with
@@ -97,14 +81,6 @@ int sr_cart_tune_rows(int bulk, int min_n);
 
 /* Workspace bytes sr_cart_normal needs for these arguments. */
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
-/* 1 if the persistent fused K1 is instantiated for an ny x nx grid. */
-int sr_fused_normal_supported(int ny, int nx);
-/* Schedule of the fused K1 (process-wide): round r runs A(r), B(r - lagB), C(r - lagC);
- * `slots` slice slots of workspace ring (lagC < slots <= 8); tile = 8 or 16 rows/columns per item. */
-int sr_fused_config(int lagB, int lagC, int slots, int tile);
-/* Diagnostics of the fused K1: dev_buf = 8 device uint64 counters (spin iterations at the
- * A-slot / B / C wait sites, then clock64 cycles spent in A / B / C items), NULL = off. */
-int sr_fused_stats(unsigned long long* dev_buf);
 
 /* K2 -- SENSE forward A x (unweighted Cartesian): per-coil centered unitary FFT
  * sampled at the trajectory bins, `SenseOperator._forward` (forward_model.py:168-172)

@@ -51,17 +51,10 @@ SIGNATURES = {
     "sr_scalar_op": [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp],
     "sr_host_vd_poisson": [_i, _i, C.c_double, _i, C.c_ulonglong, _vp],
     "sr_cart_ws_bytes": [_i, _i, _i, _i, _i],
-    "sr_fused_normal_supported": [_i, _i],
-    "sr_group_normal_supported": [_i, _i],
-    "sr_group_ngroups": [_i, _i],
-    "sr_group_select": [_i],
     "sr_cart_tune": [_i],
     "sr_cart_tune_colpf": [_i],
     "sr_cart_tune_carveout": [_i],
-    "sr_split_tune": [_i, _i],
     "sr_cart_tune_rows": [_i, _i],
-    "sr_fused_config": [_i, _i, _i, _i],
-    "sr_fused_stats": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                         _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_forward": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,

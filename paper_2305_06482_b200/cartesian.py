@@ -121,7 +121,7 @@ class CartesianKernel:
         """out = e(sum_j conj(c_j) F^H M F (c_j (x - anchor)))  (K1).
 
         chunk: None -> self.chunk; 0 -> three launches over the batch; > 0 -> three launches
-        per group of `chunk` slices; -1 -> one persistent launch (L2-resident workspace ring).
+        per group of `chunk` slices.
         """
         _no_weights(w)
         ncoils, mbs = self._maps_stride(maps)

@@ -106,11 +106,8 @@ def test_batched_normal_op_vs_oracle(cuda, dims):
     refs = [O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b])).normal(x[b]) for b in range(B)]
     for b in range(B):
         assert rel(got[b], refs[b]) < OP_TOL, b
-    # the other schedules of the same operator: chunked three-pass and the persistent launch
-    from paper_2305_06482_b200 import _lib
-    schedules = [2] + ([-1] if _lib.lib().sr_fused_normal_supported(*dims) else [])
-    schedules += [-2] if _lib.lib().sr_group_normal_supported(*dims) else []
-    for ch in schedules:
+    # the chunked three-pass schedule of the same operator
+    for ch in (2,):
         out2 = torch.full_like(xd, float("nan"))
         kern.normal(md, xd, out2, chunk=ch)
         got2 = out2.cpu().numpy()
@@ -128,68 +125,6 @@ def test_batched_normal_op_vs_oracle(cuda, dims):
         a = O.Sense(maps[b], O.CartesianKernel(dims, pts_all[b]))
         n = len(pts_all[b])
         assert rel(adj[b].cpu().numpy(), a.adjoint(y[b, :, :n].cpu().numpy().astype(np.complex128).ravel())) < OP_TOL
-
-
-@pytest.mark.parametrize("dims,B,C", [((320, 320), 4, 12), ((64, 64), 3, 5), ((256, 160), 2, 7)])
-def test_group_schedule_epilogue_and_determinism(cuda, dims, B, C):
-    """Group schedule (chunk -2): anchor + FISTA epilogue equal to the three-pass schedule,
-    slices split across CTA groups (partials combined in group order), bitwise repeatable."""
-    from paper_2305_06482_b200 import _lib
-    from paper_2305_06482_b200.cartesian import CartesianKernel
-    from paper_2305_06482_b200.plan import cartesian_plan
-    if not _lib.lib().sr_group_normal_supported(*dims):
-        pytest.skip("size not instantiated")
-    rng = np.random.default_rng(11)
-    D = dims[0] * dims[1]
-    plans = []
-    for b in range(B):
-        pts = np.argwhere(rng.random(dims) < 0.25) - np.array([n // 2 for n in dims])
-        plans.append(cartesian_plan(dims, pts))
-    kern = CartesianKernel(dims, plans)
-    t = lambda v: torch.from_numpy(v.astype(np.complex64)).cuda()  # noqa: E731
-    cplx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
-    maps = t(cplx(B, C, D) / 3)
-    z, a, d = t(cplx(B, D)), t(cplx(B, D)), t(cplx(B, D))
-    coef = torch.tensor([[-0.3 - 0.1 * b, 1.0, -0.2, 0.0] for b in range(B)], dtype=torch.float32,
-                        device="cuda")
-    outs = []
-    for ch in (0, -2, -2):
-        o = torch.full_like(z, float("nan"))
-        kern.normal(maps, z, o, anchor=a, coef=coef, u=z, d=d, chunk=ch)
-        outs.append(o.cpu().numpy())
-    assert rel(outs[1], outs[0]) < 1e-5
-    np.testing.assert_array_equal(outs[1], outs[2])
-
-
-@pytest.mark.parametrize("n,B,C", [(320, 3, 12), (256, 2, 5), (384, 1, 3)])
-def test_split_schedule_vs_oracle(cuda, n, B, C):
-    """Split-column schedule (chunk -3, cart_split.cu): the column FFT's DFT_Q step inside the
-    row passes; normal op with anchor + FISTA epilogue against the oracle and the three-pass
-    schedule, per-slice masks with duplicates-free random sampling."""
-    from paper_2305_06482_b200 import _lib  # noqa: F401
-    from paper_2305_06482_b200.cartesian import CartesianKernel
-    from paper_2305_06482_b200.plan import cartesian_plan
-    dims = (n, n)
-    rng = np.random.default_rng(23)
-    D = n * n
-    pts_l = [np.argwhere(rng.random(dims) < 0.2) - n // 2 for _ in range(B)]
-    kern = CartesianKernel(dims, [cartesian_plan(dims, p) for p in pts_l])
-    t = lambda v: torch.from_numpy(v.astype(np.complex64)).cuda()  # noqa: E731
-    cplx = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)  # noqa: E731
-    maps_h, z_h, a_h, d_h = cplx(B, C, D) / 3, cplx(B, D), cplx(B, D), cplx(B, D)
-    maps, z, a, d = t(maps_h), t(z_h), t(a_h), t(d_h)
-    out = torch.full_like(z, float("nan"))
-    kern.normal(maps, z, out, chunk=-3)
-    for b in range(B):
-        ref = O.Sense(maps_h[b], O.CartesianKernel(dims, pts_l[b])).normal(z_h[b])
-        assert rel(out[b].cpu().numpy(), ref) < OP_TOL
-    coef = torch.tensor([[-0.3 - 0.1 * b, 1.0, -0.2, 0.0] for b in range(B)], dtype=torch.float32, device="cuda")
-    outs = []
-    for ch in (0, -3):
-        o = torch.full_like(z, float("nan"))
-        kern.normal(maps, z, o, anchor=a, coef=coef, u=z, d=d, chunk=ch)
-        outs.append(o.cpu().numpy())
-    assert rel(outs[1], outs[0]) < 1e-5
 
 
 def test_fused_fista_epilogue(cuda):
