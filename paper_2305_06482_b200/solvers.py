@@ -310,8 +310,8 @@ def fista(grad, prox, L: float, x0: Image, cfg: SolverConfig, objective=None,
     t_k = 1.0
     hist = []
     iters = 0
-    v = torch.empty_like(x)
     for iters in range(1, cfg.max_iters + 1):
+        v = torch.empty_like(x)  # fresh: a caller's prox may return its argument
         lincomb(v, z, grad(z), cx=1.0, cy=-step)
         x_new = prox(v, step)
         t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_k * t_k))
