@@ -79,15 +79,6 @@ int sr_cart_tune_carveout(int pct);
  * Q >= 12, where it measured faster); rows shorter than min_n always use the copy-out. */
 int sr_cart_tune_rows(int bulk, int min_n);
 
-/* Tuning: slices per launch (chunk) from which sr_cart_normal runs the single-pass cluster
- * schedule (cart_cluster.cu: a 4-CTA cluster holds each coil image on chip; sizes 320x320,
- * 256x256, 256x160) instead of the three launches; 0 = never.  Default 16. */
-int sr_cart_tune_cluster(int min_batch);
-/* Probe only: a device buffer of 7 int64 that the cluster schedule's CTAs add their per-phase
- * SM clocks to (row IFFT + coil sum, row FFT step 1, row step 2, column DFT, exchange, column
- * IDFT, row step 2'); nullptr (default) disables it. */
-int sr_cart_cluster_profile(void* buf);
-
 /* Workspace bytes sr_cart_normal needs for these arguments. */
 long long sr_cart_ws_bytes(int batch, int ncoils, int ny, int nx, int chunk);
 

@@ -55,8 +55,6 @@ SIGNATURES = {
     "sr_cart_tune_colpf": [_i],
     "sr_cart_tune_carveout": [_i],
     "sr_cart_tune_rows": [_i, _i],
-    "sr_cart_tune_cluster": [_i],
-    "sr_cart_cluster_profile": [_vp],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                         _vp, _vp, _vp, _vp, _i, _i, _vp],
     "sr_nufft_forward": [_vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,

@@ -22,7 +22,7 @@ import math
 import sys
 from pathlib import Path
 
-SIZES = (1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 30, 32, 40, 64, 80)
+SIZES = (1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 30, 32)
 
 
 def _fmt(v: float) -> str:
