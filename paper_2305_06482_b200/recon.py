@@ -54,7 +54,9 @@ class EngineResult:
 
 
 _POWER_V0: dict = {}
-GRAPH_MIN_REPLAYED = int(os.environ.get("SR_GRAPH_MIN_REPLAYED", "400"))
+# use_graph=None: replay the outer iterations of fixed-count runs with >= 3 outers as a CUDA graph
+OUTER_GRAPH = os.environ.get("SR_OUTER_GRAPH", "1") != "0"
+GRAPH_MAX_PIXELS = 1 << 21
 
 
 def _power_start(seed: int, d: int, dev) -> torch.Tensor:
@@ -127,15 +129,11 @@ class SketchedReconEngine:
         if reg == "l1-tv":  # dual variable and scratch of the PDHG sub-solver
             self.p = torch.zeros(B, self.ndim * D, dtype=torch.complex64, device=self.dev)
             self.wbuf, self.rhs, self.xn = mk(), mk(), mk()
-        # the inner FISTA loop of every outer iteration launches the same kernels on the same
-        # buffers, so it can be captured once as a CUDA graph and replayed (t >= 2).  Capture +
-        # instantiation costs ~10 ms, saving ~50 us per inner iteration of launch overhead, so
-        # None (auto) captures only when at least GRAPH_MIN_REPLAYED inner iterations replay.
+        # every outer iteration after the first launches the same kernels on the same buffers, so a
+        # fixed-count run captures it once as a CUDA graph and replays it (run(); None = auto)
         self.use_graph = use_graph if use_graph is None else bool(use_graph)
         if self.shard is not None:
             self.use_graph = False
-        self._graph = None
-        self._smaps_buf = None
         self.step = None       # (B,) float64 device
         self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
         self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
@@ -254,24 +252,56 @@ class SketchedReconEngine:
                 break
         return it
 
-    def _fista_graphed(self, smaps, inner: int):
-        """Replay of the captured inner loop on a persistent sketched-maps buffer."""
-        if self._graph is None:
-            self._smaps_buf = smaps.clone()
-            g = torch.cuda.CUDAGraph()
-            side = torch.cuda.Stream(self.dev)
-            side.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(side), self.counter.paused():
-                # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
-                g.capture_begin()
-                self._fista(self._smaps_buf, inner)
-                g.capture_end()
-            torch.cuda.current_stream().wait_stream(side)
-            self._graph = g
+    def _step_size(self, smaps):
+        """Power iteration on this outer's sketched operator and the FISTA coefficients that follow
+        from it (coil_sketch.py:279-283); device tensors only."""
+        B = self.B
+        lam_max = self.power_lambda(smaps)
+        lip = lam_max / self.step_scale
+        step = 1.0 / lip
+        self.fcoef[:, 0] = (-step).float()
+        self.fcoef[:, 1] = 1.0
+        self.fcoef[:, 2] = (-step).float()
+        self.thresh.copy_((step * self.lam).float())
+        if self.reg == "l2":
+            if getattr(self, "l2coef", None) is None:
+                self.l2coef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+            self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
+        return lip
+
+    def _outer_body(self, mat, inner: int, tol: float, power: bool):
+        """One outer iteration of Algorithm 1 up to its objective: d = A^H r, the sketched maps of
+        `mat`, (the step size), the anchored sub-solve and the objective.  Returns (obj, finite,
+        lip or None); nothing in it reads the host when tol == 0, so it can be a CUDA graph."""
+        self.true_gradient(self.d)
+        smaps = self._sketch(mat)
+        lip = self._step_size(smaps) if power else None
+        self.anchor.copy_(self.x)
+        if self.solver == "fista":
+            self._fista(smaps, inner, tol)
+        elif self.solver == "pdhg":
+            self._pdhg(smaps, inner, tol)
         else:
-            self._smaps_buf.copy_(smaps)
-        self._graph.replay()
-        self.counter.add("coil_transform", 2 * self.chat * inner)
+            self._cg(smaps, inner)
+        finite = torch.isfinite(torch.view_as_real(self.x)).reshape(self.B, -1).all(dim=1)
+        obj = self.objective(self.x)
+        obj = torch.where(finite, obj, torch.full_like(obj, float("inf")))
+        return obj, finite, lip
+
+    def _capture_outer(self, mat_buf, inner: int, power: bool):
+        """Capture _outer_body on the persistent sketch buffer `mat_buf` as one CUDA graph (its
+        temporaries live in the graph's private pool; the engine's buffers and the kernels'
+        workspaces exist from the eager first outer, so replays touch the same memory)."""
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side), self.counter.paused():
+            # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
+            g.capture_begin()
+            outs = self._outer_body(mat_buf, inner, 0.0, power)
+            g.capture_end()
+        torch.cuda.current_stream().wait_stream(side)
+        return g, outs
 
     def _cg_solve(self, smaps, sol, rhs, shift_coef, iters: int):
         """sol = `iters` CG steps on (A_s^H A_s + shift I) sol = rhs from sol = 0 (_cg_loop,
@@ -349,6 +379,7 @@ class SketchedReconEngine:
         self.x.copy_(self.anchor)
         self.z.copy_(self.anchor)
         self.p.zero_()
+        x_buf = self.x
         for _ in range(inner):
             _lib.call("sr_tv_dual", dv.ptr(self.p), dv.ptr(self.z), self._cdims, self.ndim, 0, dv.ptr(sig_t),
                       self.lam, B, st)
@@ -363,6 +394,10 @@ class SketchedReconEngine:
             self.x, self.xn = self.xn, self.x
             if stop:
                 break
+        if self.x is not x_buf:
+            # the iterate ends in the buffer it started in (a captured outer replays on fixed pointers)
+            x_buf.copy_(self.x)
+            self.x, self.xn = x_buf, self.x
 
     # ------------------------------------------------------------ Algorithm 1
     def run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
@@ -406,35 +441,41 @@ class SketchedReconEngine:
         mats_d = torch.from_numpy(np.ascontiguousarray(np.stack(mats), dtype=np.float32)).to(self.dev)
         self.chat = mats[0].shape[0]
         t_done = 0
+        # From the second outer on, a fixed-count run replays the whole outer iteration as one CUDA
+        # graph (captured once): the host issues a sketch-row copy, the replay and the bookkeeping
+        # instead of ~150 launches per outer.  The first outer runs eagerly: it sizes every
+        # workspace and (reuse_step_size) runs the power iteration whose step the replays keep.
+        graph = self.use_graph
+        if graph is None:
+            # launch-bound problems only: a batch of large slices (config 2) gains nothing and its
+            # capture would allocate the sketched maps again in the graph's private pool
+            graph = OUTER_GRAPH and outer >= 3 and B * self.D <= GRAPH_MAX_PIXELS
+        graph = bool(graph) and deferred and self.shard is None
+        power_each = self.solver == "fista" and not reuse_step_size
+        captured = None
+        mat_buf = None
+        per_outer = None
         for t in range(1, outer + 1):
-            self.true_gradient(self.d)
-            smaps = self._sketch(mats_d[t - 1])
-            if self.solver == "fista" and (lip is None or not reuse_step_size):
-                lam_max = self.power_lambda(smaps)
-                lip = lam_max / self.step_scale
-                step = 1.0 / lip
-                self.fcoef[:, 0] = (-step).float()
-                self.fcoef[:, 1] = 1.0
-                self.fcoef[:, 2] = (-step).float()
-                self.thresh.copy_((step * self.lam).float())
-                if self.reg == "l2":
-                    self.l2coef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
-                    self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
-            self.anchor.copy_(self.x)
-            if self.solver == "fista":
-                graph = self.use_graph
-                if graph is None:
-                    graph = (outer - 2) * inner >= GRAPH_MIN_REPLAYED
-                if graph and t >= 2 and self.reg == "l1-wavelet" and tol == 0.0:
-                    self._fista_graphed(smaps, inner)
+            if graph and t >= 2:
+                if captured is None:
+                    mat_buf = mats_d[t - 1].clone()
+                    captured = self._capture_outer(mat_buf, inner, power_each)
                 else:
-                    self._fista(smaps, inner, tol)
-            elif self.solver == "pdhg":
-                self._pdhg(smaps, inner, tol)
+                    mat_buf.copy_(mats_d[t - 1])
+                captured[0].replay()
+                obj, finite, lip_t = captured[1]
+                if lip_t is not None:
+                    lip = lip_t
+                for tag, n in per_outer.items():
+                    self.counter.add(tag, n)
             else:
-                self._cg(smaps, inner)
-            finite = torch.isfinite(torch.view_as_real(self.x)).reshape(B, -1).all(dim=1)
-            obj = torch.where(finite, self.objective(self.x), torch.full_like(obj0_d, float("inf")))
+                c_before = self.counter.asdict()
+                obj, finite, lip_t = self._outer_body(mats_d[t - 1], inner, tol,
+                                                      self.solver == "fista" and (lip is None or power_each))
+                if lip_t is not None:
+                    lip = lip_t
+                c_after = self.counter.asdict()
+                per_outer = {k: v - c_before.get(k, 0) for k, v in c_after.items() if v != c_before.get(k, 0)}
             obj_hist[t - 1] = obj
             cnts.append(self.counter.value("coil_transform"))
             ev = torch.cuda.Event(enable_timing=True)

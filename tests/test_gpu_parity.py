@@ -501,9 +501,12 @@ def test_coil_compress_device_matches_host(cuda):
     assert rel(dv.to_numpy128(d0d), d0.coils) < 1e-6
 
 
-def test_graphed_inner_loop_matches_eager(cuda):
-    """The CUDA-graph replay of the inner FISTA loop launches the same kernels on the same buffers:
-    its iterates are bitwise those of the eager loop."""
+@pytest.mark.parametrize("reg,solver,reuse", [("l1-wavelet", "fista", True), ("l1-wavelet", "fista", False),
+                                               ("l2", "fista", True), ("l2", "cg", True), ("l1-tv", "pdhg", True)])
+def test_graphed_outer_loop_matches_eager(cuda, reg, solver, reuse):
+    """The CUDA-graph replay of the outer iterations (t >= 2) launches the same kernels on the same
+    buffers as the eager loop: iterates, objectives, Lipschitz constants and counters are bitwise
+    those of the eager run (every sub-solver, and the per-outer power iteration)."""
     cs, fm, lo, sk, so = _api()
     from paper_2305_06482_b200 import synth
     from paper_2305_06482_b200.cartesian import CartesianKernel
@@ -520,10 +523,12 @@ def test_graphed_inner_loop_matches_eager(cuda):
     res = []
     for graph in (False, True):
         eng = SketchedReconEngine(kern, maps, y, dims=dims, sketch=sk.SketchConfig(4, 2, 2), lam=1e-3,
-                                  reg="l1-wavelet", solver="fista", use_graph=graph)
-        res.append(eng.run(4, 5))
+                                  reg=reg, solver=solver, use_graph=graph, cg_iters=3)
+        res.append(eng.run(4, 5, reuse_step_size=reuse))
     assert torch.equal(res[0].x, res[1].x)
     np.testing.assert_array_equal(np.asarray(res[0].objectives), np.asarray(res[1].objectives))
+    np.testing.assert_array_equal(res[0].lipschitz, res[1].lipschitz)
+    assert res[0].counts == res[1].counts and res[0].per_outer_counts == res[1].per_outer_counts
 
 
 def _plan_cases():
