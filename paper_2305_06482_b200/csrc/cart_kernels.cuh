@@ -69,7 +69,7 @@ template <int P, int Q>
 __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB)
 k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
          const float2* __restrict__ maps, float2* __restrict__ ws,
-         int ncoils, int ny, long long x_bstride, long long map_bstride, int bulk) {
+         int ncoils, int ny, long long x_bstride, long long map_bstride, int bulk, int cpg) {
   using S = RowShape<P, Q>;
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   constexpr int XS = RowCfg<P, Q>::XS;
@@ -86,12 +86,14 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   const long long D = (long long)ny * N;
   const int nvalid = min(ROWS, ny - row0) * N;
   init_tw_s1<P, Q>(t1, tid, T);
+  // coils [jb, je) of this CTA (blockIdx.z = coil group: small batches spread coils over CTAs)
+  const int jb = blockIdx.z * cpg, je = min(ncoils, jb + cpg);
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
   float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   // software pipeline: coil j+1's map values are loaded while coil j is transformed
   float2 mcur[Q];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) mcur[q] = valid ? __ldg(mb + P * q) : make_float2(0.f, 0.f);
+  for (int q = 0; q < Q; ++q) mcur[q] = valid ? __ldg(mb + jb * D + P * q) : make_float2(0.f, 0.f);
   // stage u = x - anchor for the CTA's rows once (reused by every coil); all loads of a
   // thread are issued before the first use so their latencies overlap (T * Q = ROWS * N)
   {
@@ -120,11 +122,11 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
   }
   __syncthreads();
   const float2* xr = xs + lr * XS + p;
-  for (int j = 0; j < ncoils; ++j) {
+  for (int j = jb; j < je; ++j) {
     float2 r[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) r[q] = cmul(mcur[q], xr[P * q]);
-    if (j + 1 < ncoils && valid) {
+    if (j + 1 < je && valid) {
       const float2* mn = mb + (j + 1) * D;
 #pragma unroll
       for (int q = 0; q < Q; ++q) mcur[q] = __ldg(mn + P * q);
@@ -191,10 +193,10 @@ k_rowfwd(const float2* __restrict__ x, const float2* __restrict__ anchor,
 // (coef[b] = {s_acc, s_u, s_d, unused}); coef == nullptr -> out = acc.
 template <int P, int Q>
 __global__ void __launch_bounds__(RowCfg<P, Q>::T, RowCfg<P, Q>::MINB_INV)
-k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
+k_rowinv(float2* __restrict__ ws, const float2* __restrict__ maps,
          float2* __restrict__ out, int ncoils, int ny, long long x_bstride,
          long long map_bstride, const float4* __restrict__ coef,
-         const float2* __restrict__ u, const float2* __restrict__ d, float oscale) {
+         const float2* __restrict__ u, const float2* __restrict__ d, float oscale, int cpg) {
   using S = RowShapeNP<P, Q>;  // rows contiguous in shared memory: one bulk copy per row
   constexpr int N = S::N, ROWS = RowCfg<P, Q>::ROWS, T = RowCfg<P, Q>::T;
   extern __shared__ __align__(16) float2 dsm[];
@@ -211,8 +213,11 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
   float2 acc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = make_float2(0.f, 0.f);
+  // coils [jb, je) of this CTA; with several coil groups (small batches) the CTA leaves its raw
+  // partial sum in coil jb's rows of the workspace (rows only it reads) for k_rowinv_sum
+  const int jb = blockIdx.z * cpg, je = min(ncoils, jb + cpg);
   const float2* mb = maps + b * map_bstride + (long long)row * N + p;
-  const float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
+  float2* wb = ws + (long long)b * ncoils * D + (long long)row0 * N;
   const int nvalid = min(ROWS, ny - row0) * N;
   // Coil tiles are double-buffered.  With even P (16-byte aligned rows, S::VEC) every row of the
   // tile is one bulk-async copy global -> shared on the TMA unit (no register staging, no
@@ -243,13 +248,13 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
       cp_async_commit();
     }
   };
-  issue_tile(0);
-  for (int j = 0; j < ncoils; ++j) {
-    if (j + 1 < ncoils) issue_tile(j + 1);
+  issue_tile(jb);
+  for (int j = jb; j < je; ++j) {
+    if (j + 1 < je) issue_tile(j + 1);
     if constexpr (S::VEC) {
-      mbar_wait(&tbar[j & 1], (j >> 1) & 1);
+      mbar_wait(&tbar[j & 1], ((j - jb) >> 1) & 1);
     } else {
-      if (j + 1 < ncoils) cp_async_wait<1>();
+      if (j + 1 < je) cp_async_wait<1>();
       else cp_async_wait<0>();
     }
     __syncthreads();
@@ -280,6 +285,12 @@ k_rowinv(const float2* __restrict__ ws, const float2* __restrict__ maps,
     __syncthreads();  // buf (j & 1) is refilled by the prefetch issued next iteration
   }
   if (!valid) return;
+  if (gridDim.z > 1) {
+    float2* pr = wb + jb * D + (long long)lr * N + p;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) pr[P * q] = acc[q];
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = cscale(acc[q], oscale);  // 1/D of the unitary FFT pair
   const long long off = b * x_bstride + (long long)row * N + p;
@@ -552,6 +563,15 @@ int row_bulk() {
   return sr_g_row_bulk;
 }
 
+// coil groups for a row pass of `blocks` CTAs: small batches (config 0: one 256^2 slice = 32 row
+// blocks) spread their coils over CTAs so the pass covers the SMs
+inline int row_coil_groups(int blocks, int ncoils) {
+  const int target = 2 * 148;
+  if (blocks >= target) return 1;
+  const int g = (target + blocks - 1) / blocks;
+  return g < ncoils ? g : ncoils;
+}
+
 template <int P, int Q>
 int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, float2* ws,
                   int batch, int ncoils, int ny, long long xbs, long long mbs, cudaStream_t st) {
@@ -564,11 +584,35 @@ int launch_rowfwd(const float2* x, const float2* anchor, const float2* maps, flo
       return SR_ECUDA;
     configured = true;
   }
-  dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
+  const int blocks = (ny + R::ROWS - 1) / R::ROWS;
+  const int groups = row_coil_groups(blocks * batch, ncoils);
+  const int cpg = (ncoils + groups - 1) / groups;
+  dim3 grid(blocks, batch, (ncoils + cpg - 1) / cpg);
   k_rowfwd<P, Q><<<grid, R::T, R::SMEM_FWD, st>>>(x, anchor, maps, ws, ncoils, ny, xbs, mbs,
-                                                   row_bulk<P, Q>());
+                                                   row_bulk<P, Q>(), cpg);
   SR_CHECK_LAUNCH();
   return SR_OK;
+}
+
+// coil-group partial sums (k_rowinv with gridDim.z > 1) -> out, fixed group order, + epilogue
+__global__ void k_rowinv_sum(const float2* __restrict__ ws, float2* __restrict__ out, int ncoils, int cpg,
+                             int ngroups, long long D, long long x_bstride, const float4* __restrict__ coef,
+                             const float2* __restrict__ u, const float2* __restrict__ d, float oscale) {
+  const int b = blockIdx.y;
+  const float2* wb = ws + (long long)b * ncoils * D;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < D; e += (long long)gridDim.x * blockDim.x) {
+    float2 a = wb[e];
+    for (int g = 1; g < ngroups; ++g) a = cadd(a, wb[(long long)g * cpg * D + e]);
+    a = cscale(a, oscale);
+    const long long o = b * x_bstride + e;
+    if (coef) {
+      const float4 c = coef[b];
+      a = cscale(a, c.x);
+      if (u) { const float2 uu = u[o]; a.x = fmaf(c.y, uu.x, a.x); a.y = fmaf(c.y, uu.y, a.y); }
+      if (d) { const float2 dd = d[o]; a.x = fmaf(c.z, dd.x, a.x); a.y = fmaf(c.z, dd.y, a.y); }
+    }
+    out[o] = a;
+  }
 }
 
 template <int P, int Q>
@@ -584,9 +628,19 @@ int launch_rowinv(const float2* ws, const float2* maps, float2* out, int batch, 
       return SR_ECUDA;
     configured = true;
   }
-  dim3 grid((ny + R::ROWS - 1) / R::ROWS, batch);
-  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(ws, maps, out, ncoils, ny, xbs, mbs, coef, u, d, oscale);
+  const int blocks = (ny + R::ROWS - 1) / R::ROWS;
+  const int groups = row_coil_groups(blocks * batch, ncoils);
+  const int cpg = (ncoils + groups - 1) / groups, ng = (ncoils + cpg - 1) / cpg;
+  dim3 grid(blocks, batch, ng);
+  k_rowinv<P, Q><<<grid, R::T, R::SMEM_INV, st>>>(const_cast<float2*>(ws), maps, out, ncoils, ny, xbs, mbs, coef,
+                                                   u, d, oscale, cpg);
   SR_CHECK_LAUNCH();
+  if (ng > 1) {
+    const long long D = (long long)ny * P * Q;
+    dim3 g2((unsigned)((D + 255) / 256 < 1024 ? (D + 255) / 256 : 1024), batch);
+    k_rowinv_sum<<<g2, 256, 0, st>>>(ws, out, ncoils, cpg, ng, D, xbs, coef, u, d, oscale);
+    SR_CHECK_LAUNCH();
+  }
   return SR_OK;
 }
 
@@ -622,7 +676,8 @@ int launch_colnormal_t(float2* ws, const uint8_t* maskT, long long mbs, int batc
     configured = true;
   }
   if (apply_carveout(k_colnormal<P, Q, NX, PF>, carve)) return SR_ECUDA;
-  const int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
+  int jc = sr_g_col_jc < ncoils ? sr_g_col_jc : ncoils;
+  if ((NX / C::CB) * ((ncoils + jc - 1) / jc) * batch < 2 * 148) jc = 1;  // small batches: a coil per CTA
   dim3 grid(NX / C::CB, (ncoils + jc - 1) / jc, batch);
   k_colnormal<P, Q, NX, PF><<<grid, C::T, smem, st>>>(ws, maskT, mbs, ncoils, jc);
   SR_CHECK_LAUNCH();

@@ -30,6 +30,8 @@ class HostKernelAdapter:
         self.nmax = self.n_points
         self.batch = 1
         self.device = device or dv.require_cuda()
+        # the user's transform runs on the host: the engine cannot capture it in a CUDA graph
+        self.graph_capturable = False
 
     # engine / operator protocol ------------------------------------------------
     def workspace(self, ncoils: int, batch: int | None = None, chunk: int = 0, normal: bool = True):

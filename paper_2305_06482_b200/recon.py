@@ -450,7 +450,7 @@ class SketchedReconEngine:
             # launch-bound problems only: a batch of large slices (config 2) gains nothing and its
             # capture would allocate the sketched maps again in the graph's private pool
             graph = OUTER_GRAPH and outer >= 3 and B * self.D <= GRAPH_MAX_PIXELS
-        graph = bool(graph) and deferred and self.shard is None
+        graph = bool(graph) and deferred and self.shard is None and getattr(self.kernel, "graph_capturable", True)
         power_each = self.solver == "fista" and not reuse_step_size
         captured = None
         mat_buf = None
