@@ -35,6 +35,10 @@ def c64(a, device=None) -> torch.Tensor:
     device = device or require_cuda()
     if isinstance(a, torch.Tensor):
         t = a.to(device=device, dtype=torch.complex64)
+    elif isinstance(a, np.ndarray) and a.dtype == np.complex128 and a.size >= (1 << 16):
+        # large complex128 arrays (maps, k-space data): copy as they are and round on the device
+        # (same IEEE rounding as numpy's astype, without the host pass over the array)
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device).to(torch.complex64)
     else:
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex64)).to(device)
     return t.contiguous()

@@ -57,6 +57,18 @@ _POWER_V0: dict = {}
 # use_graph=None: replay the outer iterations of fixed-count runs with >= 3 outers as a CUDA graph
 OUTER_GRAPH = os.environ.get("SR_OUTER_GRAPH", "1") != "0"
 GRAPH_MAX_PIXELS = 1 << 21
+def _capture(fn, dev):
+    """Capture fn() as a CUDA graph on a side stream (private memory pool); returns (graph, fn())."""
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
+        g.capture_begin()
+        out = fn()
+        g.capture_end()
+    torch.cuda.current_stream().wait_stream(side)
+    return g, out
 
 
 def _power_start(seed: int, d: int, dev) -> torch.Tensor:
@@ -206,8 +218,9 @@ class SketchedReconEngine:
         lam = torch.zeros(self.B, dtype=torch.float64, device=self.dev)
         coef = torch.zeros(self.B, 4, dtype=torch.float32, device=self.dev)
         flags = torch.zeros(self.B, dtype=torch.int32, device=self.dev)
-        st = dv.stream()
-        for _ in range(int(iters)):
+
+        def step():
+            st = dv.stream()
             self._normal(smaps, v, w)
             _lib.call("sr_reduce", 0, dv.ptr(w), None, self.D, self.D, self.B, dv.ptr(part), dv.ptr(r0), st)
             _lib.call("sr_reduce", 1, dv.ptr(v), dv.ptr(w), self.D, self.D, self.B, dv.ptr(part), dv.ptr(r1), st)
@@ -215,7 +228,21 @@ class SketchedReconEngine:
                       dv.ptr(flags), self.B, st)
             _lib.call("sr_lincomb", dv.ptr(v), dv.ptr(w), None, None, dv.ptr(coef), 0.0, 0.0, 0.0,
                       self.D, self.D, self.B, st)
+
+        # launch-bound sizes replay one captured iteration (identical kernels on the same buffers)
+        if self._graphable() and not torch.cuda.is_current_stream_capturing() and iters > 2:
+            g, _ = _capture(step, self.dev)
+            for _ in range(int(iters)):
+                g.replay()
+        else:
+            for _ in range(int(iters)):
+                step()
         return lam
+
+    def _graphable(self) -> bool:
+        """Launch-bound problem on a device kernel without collectives: CUDA graphs pay off."""
+        auto = self.use_graph if self.use_graph is not None else (OUTER_GRAPH and self.B * self.D <= GRAPH_MAX_PIXELS)
+        return bool(auto) and self.shard is None and getattr(self.kernel, "graph_capturable", True)
 
     def _fista(self, smaps, inner: int, tol: float = 0.0):
         """Warm-started FISTA on the anchored sub-problem (coil_sketch.py:192-199, solvers.py:284-301).
@@ -290,18 +317,10 @@ class SketchedReconEngine:
 
     def _capture_outer(self, mat_buf, inner: int, power: bool):
         """Capture _outer_body on the persistent sketch buffer `mat_buf` as one CUDA graph (its
-        temporaries live in the graph's private pool; the engine's buffers and the kernels'
+        temporaries live in the shared graph pool; the engine's buffers and the kernels'
         workspaces exist from the eager first outer, so replays touch the same memory)."""
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(self.dev)
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side), self.counter.paused():
-            # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
-            g.capture_begin()
-            outs = self._outer_body(mat_buf, inner, 0.0, power)
-            g.capture_end()
-        torch.cuda.current_stream().wait_stream(side)
-        return g, outs
+        with self.counter.paused():
+            return _capture(lambda: self._outer_body(mat_buf, inner, 0.0, power), self.dev)
 
     def _cg_solve(self, smaps, sol, rhs, shift_coef, iters: int):
         """sol = `iters` CG steps on (A_s^H A_s + shift I) sol = rhs from sol = 0 (_cg_loop,

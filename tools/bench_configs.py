@@ -101,9 +101,10 @@ def run_2d(cfgid: int, with_oracle: bool):
     data = clean + synth.complex_noise(clean.shape, 0.01 * np.abs(clean).max(), rng)
     reg = so.make_regularizer("l1-wavelet", lam, shape)
     cfg = cs.CoilSketchConfig(C, sk.SketchConfig(v + s, v, s, rademacher_scale=12 ** -0.5), reg, T, K)
-    # warm-up (plans, workspaces, first-launch costs), then the timed reconstruction
+    # warm-up (plans, workspaces, first-launch costs, the first CUDA-graph captures of the process:
+    # 3 outers), then the timed reconstructions
     cs.coil_sketching_recon(fm.KSpaceData(traj, data), fm.SensitivityMaps(shape, maps),
-                            cs.CoilSketchConfig(C, cfg.sketch, reg, 1, 1), weights=weights, kernel=kern)
+                            cs.CoilSketchConfig(C, cfg.sketch, reg, 3, 1), weights=weights, kernel=kern)
     compress = "lapack" if os.environ.get("SR_HOST_COMPRESS") else "device"
     runs = []
     for _ in range(3):
