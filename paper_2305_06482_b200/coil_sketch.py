@@ -19,7 +19,7 @@ from . import _device as dv
 from .forward_model import (DensityWeights, KSpaceData, SenseOperator, SensitivityMaps, build_sense,
                             coil_compress_device, coil_compress_svd)
 from .linops import Image, make_fourier_kernel
-from .recon import DIVERGENCE_FACTOR, SketchedReconEngine
+from .recon import DIVERGENCE_FACTOR, SketchedReconEngine, _gc_paused
 from .rng import child_seed
 from .sketching import SketchConfig, SketchMatrix, apply_sketch_to_data, build_sketched_operator, gen_sketch_matrix
 from .solvers import Regularizer, SolverConfig, composite_objective, reconstruct
@@ -137,6 +137,16 @@ def coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketc
                          weights: DensityWeights | None = None, solver_cfg: SolverConfig | None = None,
                          x_ref: Image | None = None, x0: Image | None = None, method: str = "auto",
                          kernel=None, compress: str = "device") -> ReconReport:
+    """Full coil-sketched reconstruction on the device (coil_sketch.py:220-306); see
+    _coil_sketching_recon.  Python's cyclic garbage collector is paused for the call."""
+    with _gc_paused():
+        return _coil_sketching_recon(data, maps, cfg, weights, solver_cfg, x_ref, x0, method, kernel, compress)
+
+
+def _coil_sketching_recon(data: KSpaceData, maps: SensitivityMaps, cfg: CoilSketchConfig,
+                          weights: DensityWeights | None = None, solver_cfg: SolverConfig | None = None,
+                          x_ref: Image | None = None, x0: Image | None = None, method: str = "auto",
+                          kernel=None, compress: str = "device") -> ReconReport:
     """Full coil-sketched reconstruction on the device (coil_sketch.py:220-306).
 
     ``kernel`` optionally injects the Fourier kernel (e.g. a GriddedKernel with

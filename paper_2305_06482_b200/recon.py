@@ -19,7 +19,9 @@ Counters follow the reference tally per slice: 2*C0 per true gradient,
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import gc
 
 import math
 import os
@@ -57,10 +59,29 @@ _POWER_V0: dict = {}
 # use_graph=None: replay the outer iterations of fixed-count runs with >= 3 outers as a CUDA graph
 OUTER_GRAPH = os.environ.get("SR_OUTER_GRAPH", "1") != "0"
 GRAPH_MAX_PIXELS = 1 << 21
+@contextlib.contextmanager
+def _gc_paused():
+    """Python's cyclic collector off for the duration of a reconstruction: a full collection walks
+    every tracked object of the process (~185 K with torch imported, ~33 ms) and lands at a random
+    point of the launch stream; the engine itself creates almost no cyclic garbage."""
+    was = gc.isenabled()
+    gc.disable()
+    try:
+        yield
+    finally:
+        if was:
+            gc.enable()
+
+
+_SIDE_STREAMS: dict = {}
+
+
 def _capture(fn, dev):
     """Capture fn() as a CUDA graph on a side stream (private memory pool); returns (graph, fn())."""
     g = torch.cuda.CUDAGraph()
-    side = torch.cuda.Stream(dev)
+    side = _SIDE_STREAMS.get(str(dev))
+    if side is None:
+        side = _SIDE_STREAMS[str(dev)] = torch.cuda.Stream(dev)
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
         # capture_begin/end directly: torch.cuda.graph() would empty the allocator cache
@@ -149,8 +170,22 @@ class SketchedReconEngine:
         self.step = None       # (B,) float64 device
         self.fcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
         self.thresh = torch.zeros(B, dtype=torch.float32, device=self.dev)
+        self._bufs: dict = {}
 
     # ------------------------------------------------------------ pieces
+    def _buf(self, name: str, shape, dtype, fill=None) -> torch.Tensor:
+        """Persistent scratch tensor of the engine (allocated on first use, reused after): the
+        outer iteration allocates nothing, so its CUDA graph owns no pool memory (freeing a graph's
+        private pool synchronises the device whenever the garbage collector gets to it)."""
+        shape = tuple(int(v) for v in shape)
+        t = self._bufs.get(name)
+        if t is None or tuple(t.shape) != shape or t.dtype != dtype:
+            t = torch.empty(shape, dtype=dtype, device=self.dev)
+            if fill is not None:
+                t.fill_(fill)
+            self._bufs[name] = t
+        return t
+
     def _normal(self, maps, x, out, anchor=None, coef=None, u=None, d=None):
         if self.shard is None:
             return self.kernel.normal(maps, x, out, w=self.sqrt_w, anchor=anchor, coef=coef, u=u, d=d)
@@ -170,7 +205,8 @@ class SketchedReconEngine:
     def _sketch(self, mat: np.ndarray) -> torch.Tensor:
         """This rank's rows of S^t @ maps0 (all rows without sharding)."""
         if self.shard is None:
-            return coil_contract(self.maps0, mat)
+            return coil_contract(self.maps0, mat, out=self._buf("smaps", (self.B, mat.shape[-2], self.D),
+                                                                   torch.complex64))
         lo, hi = self.shard.coils(mat.shape[0])
         if hi == lo:
             return torch.zeros(self.B, 0, self.D, dtype=torch.complex64, device=self.dev)
@@ -178,23 +214,45 @@ class SketchedReconEngine:
 
     def objective(self, x) -> torch.Tensor:
         """Per-slice 0.5||A x - y||^2 + g(x) (float64 device); leaves A x - y in self.r."""
+        return self._objective_into(x, torch.empty(self.B, dtype=torch.float64, device=self.dev))
+
+    def _objective_into(self, x, out) -> torch.Tensor:
+        """objective(x) written into `out` (B,) with the engine's scratch only (no allocation);
+        the same operations in the same order as the reference-shaped formula."""
+        B = self.B
         if self.maps_full.shape[1] > 0:
             self.kernel.forward(self.maps_full, x, self.r, ymeas=self.y, partial=self.partial, w=self.sqrt_w)
         else:
             self.partial.zero_()
         if self.shard is not None:
             self.shard.all_reduce_(self.partial)
-        obj = 0.5 * self.partial.reshape(self.B, -1).sum(dim=1)
+        torch.sum(self.partial.view(B, -1), dim=1, out=out)
+        out.mul_(0.5)
         if self.lam != 0.0:
+            reg = self._buf("obj_reg", (B,), torch.float64)
             if self.reg == "l1-wavelet":
-                obj = obj + self.lam * self.wav.l1_norm(x)
+                self.wav.l1_norm(x, out=reg, tmp=self._buf("obj_tmp", (B,), torch.float64))
+                reg.mul_(self.lam)
             elif self.reg == "l1-tv":
                 _lib.call("sr_tv_dual", dv.ptr(self.p), dv.ptr(x), self._cdims, self.ndim, 1, None, 0.0, self.B,
                           dv.stream())
-                obj = obj + self.lam * _abs_sum(self.p)
+                self._reduce_into(2, self.p, reg)
+                reg.mul_(self.lam)
             else:
-                obj = obj + 0.5 * self.lam * _norm2(x)
-        return obj
+                self._reduce_into(0, x, reg)
+                reg.mul_(0.5 * self.lam)
+            out.add_(reg)
+        return out
+
+    def _reduce_into(self, mode: int, a, out) -> torch.Tensor:
+        """out (B,) = the fixed-order device reduction `mode` of a (B, n) (sr_reduce), no allocation."""
+        n = a.numel() // self.B
+        nparts = _lib.lib().sr_reduce_nparts()
+        part = self._buf("red_part", (self.B, nparts, 2), torch.float64)
+        res = self._buf("red_res", (self.B, 2), torch.float64)
+        _lib.call("sr_reduce", mode, dv.ptr(a), None, n, n, self.B, dv.ptr(part), dv.ptr(res), dv.stream())
+        out.copy_(res[:, 0])
+        return out
 
     def true_gradient(self, out):
         """d = A^H r with r = A x - y from the last objective (coil_sketch.py:123-126)."""
@@ -209,15 +267,20 @@ class SketchedReconEngine:
 
     def power_lambda(self, smaps, iters: int = 30, seed: int = 0) -> torch.Tensor:
         """lambda_max(A_s^H A_s) per slice (linops.py:766-782), counters paused."""
-        v = _power_start(seed, self.D, self.dev).repeat(self.B, 1)  # a copy: v is updated in place
-        w = torch.empty_like(v)
+        B, D = self.B, self.D
+        v = self._buf("pw_v", (B, D), torch.complex64)
+        v.copy_(_power_start(seed, D, self.dev).expand(B, D))  # v is updated in place
+        w = self._buf("pw_w", (B, D), torch.complex64)
         nparts = _lib.lib().sr_reduce_nparts()
-        part = torch.empty(self.B, nparts, 2, dtype=torch.float64, device=self.dev)
-        r0 = torch.empty(self.B, 2, dtype=torch.float64, device=self.dev)
-        r1 = torch.empty_like(r0)
-        lam = torch.zeros(self.B, dtype=torch.float64, device=self.dev)
-        coef = torch.zeros(self.B, 4, dtype=torch.float32, device=self.dev)
-        flags = torch.zeros(self.B, dtype=torch.int32, device=self.dev)
+        part = self._buf("pw_part", (B, nparts, 2), torch.float64)
+        r0 = self._buf("pw_r0", (B, 2), torch.float64)
+        r1 = self._buf("pw_r1", (B, 2), torch.float64)
+        lam = self._buf("pw_lam", (B,), torch.float64)
+        lam.zero_()
+        coef = self._buf("pw_coef", (B, 4), torch.float32)
+        coef.zero_()
+        flags = self._buf("pw_flags", (B,), torch.int32)
+        flags.zero_()
 
         def step():
             st = dv.stream()
@@ -283,17 +346,21 @@ class SketchedReconEngine:
         """Power iteration on this outer's sketched operator and the FISTA coefficients that follow
         from it (coil_sketch.py:279-283); device tensors only."""
         B = self.B
+        f64 = torch.float64
         lam_max = self.power_lambda(smaps)
-        lip = lam_max / self.step_scale
-        step = 1.0 / lip
-        self.fcoef[:, 0] = (-step).float()
+        lip = torch.div(lam_max, self.step_scale, out=self._buf("st_lip", (B,), f64))
+        step = torch.reciprocal(lip, out=self._buf("st_step", (B,), f64))
+        t = torch.neg(step, out=self._buf("st_t", (B,), f64))
+        self.fcoef[:, 0] = t
         self.fcoef[:, 1] = 1.0
-        self.fcoef[:, 2] = (-step).float()
-        self.thresh.copy_((step * self.lam).float())
+        self.fcoef[:, 2] = t
+        self.thresh.copy_(torch.mul(step, self.lam, out=t))
         if self.reg == "l2":
             if getattr(self, "l2coef", None) is None:
                 self.l2coef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
-            self.l2coef[:, 0] = (1.0 / (1.0 + step * self.lam)).float()
+            torch.mul(step, self.lam, out=t)
+            t.add_(1.0)
+            self.l2coef[:, 0] = torch.reciprocal(t, out=t)
         return lip
 
     def _outer_body(self, mat, inner: int, tol: float, power: bool):
@@ -310,9 +377,13 @@ class SketchedReconEngine:
             self._pdhg(smaps, inner, tol)
         else:
             self._cg(smaps, inner)
-        finite = torch.isfinite(torch.view_as_real(self.x)).reshape(self.B, -1).all(dim=1)
-        obj = self.objective(self.x)
-        obj = torch.where(finite, obj, torch.full_like(obj, float("inf")))
+        # x is finite iff sum |x|^2 is (fp64 accumulation of float32 squares cannot overflow)
+        B = self.B
+        n2 = self._reduce_into(0, self.x, self._buf("x_norm2", (B,), torch.float64))
+        finite = torch.lt(n2, float("inf"), out=self._buf("x_finite", (B,), torch.bool))
+        obj = self._objective_into(self.x, self._buf("obj_val", (B,), torch.float64))
+        obj = torch.where(finite, obj, self._buf("obj_inf", (B,), torch.float64, fill=float("inf")),
+                          out=self._buf("obj_out", (B,), torch.float64))
         return obj, finite, lip
 
     def _capture_outer(self, mat_buf, inner: int, power: bool):
@@ -331,14 +402,17 @@ class SketchedReconEngine:
         loop breaks (state kept on the device, no host sync)."""
         B, D, st = self.B, self.D, dv.stream()
         sol.zero_()
-        r = rhs.clone()
-        p = r.clone()
-        mp = torch.empty_like(r)
+        r = self._buf("cg_r", rhs.shape, rhs.dtype)
+        r.copy_(rhs)
+        p = self._buf("cg_p", rhs.shape, rhs.dtype)
+        p.copy_(r)
+        mp = self._buf("cg_mp", rhs.shape, rhs.dtype)
         nparts = _lib.lib().sr_reduce_nparts()
-        pdot = torch.empty(B, nparts, 2, dtype=torch.float64, device=self.dev)
-        prs = torch.empty_like(pdot)
-        rs = torch.empty(B, 2, dtype=torch.float64, device=self.dev)
-        state = torch.zeros(B, 4, dtype=torch.float64, device=self.dev)
+        pdot = self._buf("cg_pdot", (B, nparts, 2), torch.float64)
+        prs = self._buf("cg_prs", (B, nparts, 2), torch.float64)
+        rs = self._buf("cg_rs", (B, 2), torch.float64)
+        state = self._buf("cg_state", (B, 4), torch.float64)
+        state.zero_()
         _lib.call("sr_reduce", 0, dv.ptr(r), None, D, D, B, dv.ptr(pdot), dv.ptr(rs), st)
         state[:, 0] = rs[:, 0]
         state[:, 2] = 1.0
@@ -352,10 +426,12 @@ class SketchedReconEngine:
     def _cg(self, smaps, inner: int):
         """(A_s^H A_s + lam I) delta = -d - lam x^t, x = x^t + delta (coil_sketch.py:182-191)."""
         B, D = self.B, self.D
-        delta = torch.zeros_like(self.x)
-        rhs = torch.empty_like(self.x)
+        delta = self._buf("cgo_delta", self.x.shape, self.x.dtype)
+        delta.zero_()
+        rhs = self._buf("cgo_rhs", self.x.shape, self.x.dtype)
         _lincomb(rhs, self.d, self.anchor, None, -1.0, -self.lam, 0.0, B, D)
-        lcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        lcoef = self._buf("cgo_lcoef", (B, 4), torch.float32)
+        lcoef.zero_()
         lcoef[:, 0] = 1.0
         lcoef[:, 1] = self.lam
         self._cg_solve(smaps, delta, rhs, lcoef, inner)
@@ -387,12 +463,16 @@ class SketchedReconEngine:
         ratio = math.sqrt(self.pdhg_ratio)
         sigma = ratio / norm_k * self.step_scale
         tau = 1.0 / (ratio * norm_k) * self.step_scale
-        sig_t = torch.full((B,), sigma, dtype=torch.float32, device=self.dev)
-        tau_t = torch.full((B,), tau, dtype=torch.float32, device=self.dev)
-        shift = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        sig_t = self._buf("pd_sig", (B,), torch.float32)
+        sig_t.fill_(sigma)
+        tau_t = self._buf("pd_tau", (B,), torch.float32)
+        tau_t.fill_(tau)
+        shift = self._buf("pd_shift", (B, 4), torch.float32)
+        shift.zero_()
         shift[:, 0] = 1.0
         shift[:, 1] = 1.0 / tau
-        rcoef = torch.zeros(B, 4, dtype=torch.float32, device=self.dev)
+        rcoef = self._buf("pd_rcoef", (B, 4), torch.float32)
+        rcoef.zero_()
         rcoef[:, 0] = -1.0
         rcoef[:, 2] = -1.0
         self.x.copy_(self.anchor)
@@ -421,6 +501,12 @@ class SketchedReconEngine:
     # ------------------------------------------------------------ Algorithm 1
     def run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
             x_ref: torch.Tensor | None = None, tol: float = 0.0, reuse_step_size: bool = True) -> EngineResult:
+        """Algorithm 1 (see _run), with the Python cyclic garbage collector paused."""
+        with _gc_paused():
+            return self._run(outer, inner, x0=x0, x_ref=x_ref, tol=tol, reuse_step_size=reuse_step_size)
+
+    def _run(self, outer: int, inner: int, x0: torch.Tensor | None = None,
+             x_ref: torch.Tensor | None = None, tol: float = 0.0, reuse_step_size: bool = True) -> EngineResult:
         """Algorithm 1 (coil_sketch.py:220-306).  tol > 0: FISTA inner solves stop on the relative
         change (solvers.py:300; B = 1); reuse_step_size=False re-runs the power iteration on
         every outer's sketched operator (coil_sketch.py:281)."""

@@ -138,14 +138,21 @@ class WaveletEngine:
                 self._syn(self.buf[l % 2], dst, l)
         return out
 
-    def l1_norm(self, x) -> torch.Tensor:
-        """sum |Psi x| per slice as a (B,) float64 device tensor (no host sync)."""
+    def l1_norm(self, x, out=None, tmp=None) -> torch.Tensor:
+        """sum |Psi x| per slice as a (B,) float64 device tensor (no host sync).  With `out` and `tmp`
+        ((B,) float64) nothing is allocated: the per-level block sums are added in level order, as
+        the generator sum does."""
         src = x
         for l in range(self.levels):
             dst = self.buf[l % 2]
             self._ana(src, dst, l, None, -1.0, self.l1parts[l])
             src = dst
-        return sum(p.sum(dim=1) for p in self.l1parts)
+        if out is None:
+            return sum(p.sum(dim=1) for p in self.l1parts)
+        torch.sum(self.l1parts[0], dim=1, out=out)
+        for p in self.l1parts[1:]:
+            out.add_(torch.sum(p, dim=1, out=tmp))
+        return out
 
     # ------------------------------------------------- reference-layout API
     def _corner(self, t, l):

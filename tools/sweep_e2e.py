@@ -24,10 +24,12 @@ def main():
         ch = [int(v) for v in c.split("/")] if "/" in c else int(c)
         lanes = int(lanes)
         steps = 20
-        t = bench.time_applies(lambda: kern.normal_host(smaps, x_host, out_host, chunks=ch, buffers=stage,
-                                                        lanes=lanes), steps, 3, torch.cuda.synchronize)
-        print(json.dumps({"chunks": ch, "lanes": lanes, "e2e_applies_per_s": steps / t, "ms": t / steps * 1e3}),
-              flush=True)
+        for ov in (False, True):
+            t = bench.time_applies(lambda: kern.normal_host(smaps, x_host, out_host, chunks=ch, buffers=stage,
+                                                            lanes=lanes, overlap_prev=ov), steps, 3,
+                                   torch.cuda.synchronize)
+            print(json.dumps({"chunks": ch, "lanes": lanes, "overlap_prev": ov, "e2e_applies_per_s": steps / t,
+                              "ms": t / steps * 1e3}), flush=True)
     # raw copy bandwidth
     xd = stage[0]
     for name, fn in [("h2d", lambda: xd.copy_(x_host, non_blocking=True)),

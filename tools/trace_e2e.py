@@ -23,11 +23,11 @@ def main():
     out_host = torch.empty_like(x_host).pin_memory()
     stage = (torch.empty_like(x), torch.empty_like(x))
     for _ in range(3):
-        kern.normal_host(smaps, x_host, out_host, chunks=chunks, buffers=stage, lanes=lanes)
+        kern.normal_host(smaps, x_host, out_host, chunks=chunks, buffers=stage, lanes=lanes, overlap_prev=True)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(3):
-            kern.normal_host(smaps, x_host, out_host, chunks=chunks, buffers=stage, lanes=lanes)
+            kern.normal_host(smaps, x_host, out_host, chunks=chunks, buffers=stage, lanes=lanes, overlap_prev=True)
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     evs.sort(key=lambda e: e.time_range.start)
