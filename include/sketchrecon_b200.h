@@ -251,6 +251,22 @@ int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, i
                     const float* frac, const float* wgt, long long nsamples, sr_c64* out,
                     sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, const int* chunks,
                     int nchunks, int binsize, void* stream);
+/* sr_nufft_normal in two parts for the coil-sharded pipeline (config 4): _head runs the embed, the
+ * forward passes, the gridding and the axis-0 inverse pass into `grids`; _tail finishes image
+ * planes i0 in [i0a, i0b) only (remaining inverse passes, crop, conjugate coil sum, epilogue), so
+ * a caller can all-reduce one slab of the coil sum while the next slab computes.  head + tail over
+ * [0, dims[0]) == sr_nufft_normal.  Partial slabs need dims[0] * dims[1] >= 9472 image rows
+ * (sr_nufft_normal_slabs_ok); otherwise _tail returns SR_EUNSUPPORTED for a partial slab. */
+int sr_nufft_normal_head(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
+                         const int* dims, const int* gdims, const float* betas, int width, const float* ia0,
+                         const float* ia1, const float* ia2, const int* base, const float* frac, const float* wgt,
+                         long long nsamples, sr_c64* grids, const int* chunks, int nchunks, int binsize,
+                         void* stream);
+int sr_nufft_normal_tail(const sr_c64* maps, int ncoils, const int* dims, const int* gdims, const float* betas,
+                         int width, const float* ia0, const float* ia1, const float* ia2, sr_c64* out,
+                         sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, int i0a, int i0b,
+                         void* stream);
+int sr_nufft_normal_slabs_ok(const int* dims);
 int sr_nufft_forward(const sr_c64* x, const sr_c64* maps, int ncoils, const int* dims, const int* gdims,
                      const float* betas, int width, const float* ia0, const float* ia1, const float* ia2,
                      const int* base, const float* frac, const float* sqrtw, const int* orig,

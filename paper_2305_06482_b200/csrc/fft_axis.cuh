@@ -28,12 +28,19 @@ static __device__ __forceinline__ int ax_wrap(int i, int n, int g) {
 struct AxPrune {
   int nin, nout;  // extents along the FFT axis (== N: no pruning)
   int on, og;     // live / total planes of the axis just outside (on == og: all planes)
+  int oa = 0;     // first live image plane (a slab of the image planes: oa .. oa + on of onf)
+  int onf = 0;    // image planes of that axis when only a slab is live (0: on)
   __device__ __forceinline__ bool in(int k, int N) const { return nin == N || ax_inside(k, nin, N); }
   __device__ __forceinline__ bool out(int k, int N) const { return nout == N || ax_inside(k, nout, N); }
   __device__ __forceinline__ long long plane(long long o) const {
-    if (on == og) return o;
+    if (onf == 0) {
+      if (on == og) return o;
+      const long long j = o / on;
+      return j * og + ax_wrap((int)(o - j * on), on, og);
+    }
     const long long j = o / on;
-    return j * og + ax_wrap((int)(o - j * on), on, og);
+    const int i = oa + (int)(o - j * on);
+    return j * og + (onf == og ? i : ax_wrap(i, onf, og));
   }
 };
 
@@ -58,6 +65,9 @@ struct RowGeom {
   const float4* coef;
   const float2* u;
   const float2* d;
+  // inverse row pass: only the image planes i0 in [i0a, i0b) (i0b < 0: all n0) -- one slab of the
+  // coil-sharded pipeline whose coil sum is all-reduced while the next slab computes
+  int i0a = 0, i0b = -1;
 };
 
 
@@ -378,14 +388,15 @@ k_rows_crop(const RowGeom rg) {
   float2* tw = dsm;
   float2* bufs = dsm + N;  // two row tiles: coil j+1 streams in (cp.async) while coil j transforms
   const int tid = threadIdx.x;
-  const long long nrows = (long long)rg.n0 * rg.n1;
+  const int i0a = rg.i0a, i0b = rg.i0b < 0 ? rg.n0 : rg.i0b;
+  const long long nrows = (long long)(i0b - i0a) * rg.n1;
   const long long row0 = (long long)blockIdx.x * ROWS;
   const int lr = tid / P, p = tid % P;
   init_tw_s2<P, Q>(tw, tid, T);
   const long long rid = row0 + lr;
   const bool valid = rid < nrows;
-  const int i0 = valid ? (int)(rid / rg.n1) : 0;
-  const int i1 = valid ? (int)(rid - (long long)i0 * rg.n1) : 0;
+  const int i0 = valid ? i0a + (int)(rid / rg.n1) : 0;
+  const int i1 = valid ? (int)(rid - (long long)(i0 - i0a) * rg.n1) : 0;
   if (p == 0) rbase[lr] = ((long long)ax_wrap(i0, rg.n0, rg.g0) * rg.g1 + ax_wrap(i1, rg.n1, rg.g1)) * N;
   const long long pixrow = ((long long)i0 * rg.n1 + i1) * rg.n2;
   const int h2 = rg.n2 >> 1;
@@ -475,7 +486,9 @@ int launch_row_fused(const RowGeom& rg, cudaStream_t st) {
       return SR_ECUDA;
     cfg = true;
   }
-  const long long nrows = INV ? (long long)rg.n0 * rg.n1 : (long long)rg.ncoils * rg.n0 * rg.n1;
+  const int nplanes = INV ? (rg.i0b < 0 ? rg.n0 : rg.i0b) - rg.i0a : rg.n0;
+  const long long nrows = INV ? (long long)nplanes * rg.n1 : (long long)rg.ncoils * rg.n0 * rg.n1;
+  if (nrows <= 0) return SR_OK;
   const long long nblk = (nrows + A::ROWS - 1) / A::ROWS;
   if (nblk > 0x7fffffffLL) return SR_EINVAL;
   kern<<<(unsigned)nblk, A::T, smem, st>>>(rg);

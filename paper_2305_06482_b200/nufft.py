@@ -295,6 +295,25 @@ class GriddedKernel:
                   dv.stream())
         return out
 
+    def slab_planes(self) -> int:
+        """Image planes along axis 0 that normal_slabs can split (0: no split for this grid)."""
+        return int(self.dims3[0]) if _lib.lib().sr_nufft_normal_slabs_ok(self.dims3.data_ptr()) else 0
+
+    def normal_slabs(self, maps, x, out, bounds, on_slab, *, anchor=None, coef=None, u=None, d=None, w=None):
+        """normal() with the inverse tail issued one slab of image planes at a time: bounds =
+        [(i0a, i0b), ...] covering [0, n0); after each slab's launches, on_slab(i0a, i0b) is called
+        (the coil-sharded engine starts that slab's all-reduce there while the next slab computes)."""
+        C = self._maps(maps)
+        grids = self.workspace(C, normal=True)
+        _lib.call("sr_nufft_normal_head", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), C, *self._geom(),
+                  dv.ptr(self.base), dv.ptr(self.frac), dv.ptr(self._weights(w, True)), self.n_points,
+                  dv.ptr(grids), *self._bins(), dv.stream())
+        for a, b in bounds:
+            _lib.call("sr_nufft_normal_tail", dv.ptr(maps), C, *self._geom(), dv.ptr(out), dv.ptr(grids),
+                      dv.ptr(coef), dv.ptr(u), dv.ptr(d), int(a), int(b), dv.stream())
+            on_slab(a, b)
+        return out
+
     def forward(self, maps, x, y=None, *, ymeas=None, partial=None, partial_blocks=None, w=None):
         C = self._maps(maps)
         if y is None:

@@ -55,6 +55,23 @@ class CoilShard:
                 dist.all_reduce(t, group=self.group)
         return t
 
+    def all_reduce_async(self, t: torch.Tensor):
+        """Start an in-place sum over ranks of a contiguous tensor (view); returns a handle whose
+        .wait() makes the current stream wait for the collective.  NCCL runs it on its own stream,
+        so kernels queued on the current stream after this call overlap it."""
+        import torch.distributed as dist
+        if self.world == 1:
+            return _Done()
+        v = torch.view_as_real(t) if t.is_complex() else t
+        if not v.is_contiguous():
+            raise ValueError("all_reduce_async needs a contiguous view")
+        return dist.all_reduce(v, group=self.group, async_op=True)
+
+
+class _Done:
+    def wait(self):
+        return True
+
 
 def sharded_normal(partial_fn, x: torch.Tensor, shard: CoilShard) -> torch.Tensor:
     """sum_ranks partial_fn(x): each rank applies A_r^H A_r over its coils, then all-reduce."""

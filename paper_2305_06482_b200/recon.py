@@ -59,6 +59,8 @@ _POWER_V0: dict = {}
 # use_graph=None: replay the outer iterations of fixed-count runs with >= 3 outers as a CUDA graph
 OUTER_GRAPH = os.environ.get("SR_OUTER_GRAPH", "1") != "0"
 GRAPH_MAX_PIXELS = 1 << 21
+# image-plane slabs of the coil-sharded NUFFT normal op whose all-reduces overlap the next slab
+SHARD_SLABS = 4
 @contextlib.contextmanager
 def _gc_paused():
     """Python's cyclic collector off for the duration of a reconstruction: a full collection walks
@@ -189,12 +191,33 @@ class SketchedReconEngine:
     def _normal(self, maps, x, out, anchor=None, coef=None, u=None, d=None):
         if self.shard is None:
             return self.kernel.normal(maps, x, out, w=self.sqrt_w, anchor=anchor, coef=coef, u=u, d=d)
-        # partial over this rank's sketched coils, all-reduce, then the epilogue
-        if maps.shape[1] > 0:
-            self.kernel.normal(maps, x, self.tmp, w=self.sqrt_w, anchor=anchor)
+        # partial over this rank's sketched coils, all-reduce, then the epilogue.  With a kernel
+        # that finishes its image in slabs of planes (3-D NUFFT), each slab's all-reduce starts as
+        # soon as its launches are queued and runs under the next slab's inverse passes.
+        nplanes = self.kernel.slab_planes() if hasattr(self.kernel, "slab_planes") else 0
+        if nplanes >= 2 * SHARD_SLABS and self.shard.world > 1 and self.B == 1:
+            # every rank issues the same slab collectives (a rank without sketched coils sends zeros)
+            bounds = [(nplanes * k // SHARD_SLABS, nplanes * (k + 1) // SHARD_SLABS) for k in range(SHARD_SLABS)]
+            plane = self.D // nplanes
+            works = []
+
+            def slab_done(a, b):
+                works.append(self.shard.all_reduce_async(self.tmp[:, a * plane:b * plane]))
+
+            if maps.shape[1] > 0:
+                self.kernel.normal_slabs(maps, x, self.tmp, bounds, slab_done, w=self.sqrt_w, anchor=anchor)
+            else:
+                self.tmp.zero_()
+                for a, b in bounds:
+                    slab_done(a, b)
+            for wk in works:
+                wk.wait()
         else:
-            self.tmp.zero_()
-        self.shard.all_reduce_(self.tmp)
+            if maps.shape[1] > 0:
+                self.kernel.normal(maps, x, self.tmp, w=self.sqrt_w, anchor=anchor)
+            else:
+                self.tmp.zero_()
+            self.shard.all_reduce_(self.tmp)
         if coef is None:
             out.copy_(self.tmp)
         else:

@@ -93,3 +93,101 @@ def test_coil_sharded_engine_world2_matches_unsharded(cuda):
         assert cnt == int(ref.counts["coil_transform"])
     # both ranks hold the same (replicated) image
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+# --- slab-pipelined all-reduce (the coil sum of a 3-D NUFFT normal op finished one slab of image
+# planes at a time, each slab's all-reduce overlapping the next slab's inverse passes)
+SLAB_DIMS = (128, 96, 32)  # 128 x 96 = 12288 image rows: the fused row pass, so slabs apply
+
+
+def _slab_problem(dev, coils=6):
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    pts = synth.cones_3d(SLAB_DIMS, n_readouts=300, n_samples=200)
+    kern = GriddedKernel(SLAB_DIMS, pts, 1.25, 4)
+    g = torch.Generator(dev).manual_seed(7)
+    D = kern.D
+    maps = torch.randn(1, coils, D, dtype=torch.complex64, device=dev, generator=g) * 0.3
+    x = torch.randn(1, D, dtype=torch.complex64, device=dev, generator=g)
+    return kern, maps, x, pts
+
+
+def test_nufft_normal_slabs_equal_normal(cuda):
+    """head + per-slab tails == the one-call normal op (same kernels per output row; the gridding
+    flush's float atomics make two calls of either agree to fp32 rounding, not bitwise), with and
+    without the solver epilogue; a partial slab on a grid too small for it is refused."""
+    kern, maps, x, _ = _slab_problem(cuda)
+    assert kern.slab_planes() == SLAB_DIMS[0]
+    a = torch.randn_like(x) * 0.1
+    coef = torch.tensor([[0.5, -1.0, 0.25, 0.0]], device=cuda)
+    dd = torch.randn_like(x)
+    for kw in ({}, dict(anchor=a, coef=coef, u=x, d=dd)):
+        ref = torch.empty_like(x)
+        kern.normal(maps, x, ref, **kw)
+        for nslab in (1, 3, 4):
+            n0 = SLAB_DIMS[0]
+            bounds = [(n0 * k // nslab, n0 * (k + 1) // nslab) for k in range(nslab)]
+            seen = []
+            out = torch.full_like(x, float("nan"))
+            kern.normal_slabs(maps, x, out, bounds, lambda lo, hi: seen.append((lo, hi)), **kw)
+            assert seen == bounds
+            err = float(torch.linalg.vector_norm(out - ref) / torch.linalg.vector_norm(ref))
+            assert err < 1e-6, (kw.keys(), nslab, err)
+    from paper_2305_06482_b200 import synth
+    from paper_2305_06482_b200.nufft import GriddedKernel
+    small = GriddedKernel((16, 24, 16), synth.cones_3d((16, 24, 16), n_readouts=40, n_samples=60), 1.25, 4)
+    assert small.slab_planes() == 0
+    m2 = torch.ones(1, 1, small.D, dtype=torch.complex64, device=cuda)
+    x2 = torch.ones(1, small.D, dtype=torch.complex64, device=cuda)
+    with pytest.raises(ValueError):
+        small.normal_slabs(m2, x2, torch.empty_like(x2), [(0, 10), (10, 20)], lambda lo, hi: None)
+
+
+def _slab_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_06482_b200.parallel_recon import CoilShard
+        res = _slab_engine(torch.device("cuda", 0), CoilShard(rank, world))
+        q.put((rank, res.x.cpu().numpy(), np.asarray(res.objectives), float(res.lipschitz[0])))
+    except Exception as e:
+        q.put((rank, repr(e), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _slab_engine(dev, shard):
+    from paper_2305_06482_b200.recon import SketchedReconEngine
+    from paper_2305_06482_b200.sketching import SketchConfig
+    kern, maps, x, pts = _slab_problem(dev, coils=8)
+    g = torch.Generator(dev).manual_seed(11)
+    y = torch.zeros(1, 8, kern.nmax, dtype=torch.complex64, device=dev)
+    y[:, :, : kern.n_points] = torch.randn(1, 8, kern.n_points, dtype=torch.complex64, device=dev, generator=g)
+    eng = SketchedReconEngine(kern, maps, y, dims=SLAB_DIMS, sketch=SketchConfig(4, 2, 2), lam=1e-3, shard=shard)
+    return eng.run(2, 3)
+
+
+def test_coil_sharded_slab_pipeline_world2_matches_unsharded(cuda):
+    """Two gloo ranks run the engine whose sketched normal op all-reduces its coil sum slab by slab
+    (async collectives); the image, objectives and step size match the unsharded engine."""
+    import torch.multiprocessing as mp
+    ref = _slab_engine(cuda, None)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    xr = ref.x.cpu().numpy()
+    for rank, x, objs, lip in outs:
+        assert not isinstance(x, str), x
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-5, rank
+        np.testing.assert_allclose(objs, ref.objectives, rtol=1e-5)
+        assert abs(lip - float(ref.lipschitz[0])) < 1e-5 * abs(lip)
