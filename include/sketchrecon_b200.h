@@ -281,8 +281,9 @@ int sr_nufft_partial_blocks(long long nsamples);
 /* 3-D Cartesian mask kernel (_CartesianMaskKernel on a 3-D grid, linops.py:332-364, which the
  * 2-D K1/K2 kernels do not cover): the grid pipeline of the NUFFT entries with g = n and unit
  * apodisation.  dims (3, HOST ints, axes with sr_fft_size_supported lengths); ones0..2 device
- * float vectors of ones (lengths dims[a]); spos (N) int32 perm-layout offset of each sample,
- * sum_a perm(f_a mod n_a) * stride_a; mask (n0 n1 n2) uint8 sampled-bin indicator in the same
+ * float vectors of ones (lengths dims[a]); spos (N) int32 grid offset of each sample,
+ * perm(f_0) n1 n2 + perm(f_1) n2 + f_2 (f_a mod n_a; axes 0-1 perm order, the contiguous axis 2
+ * natural); mask (n0 n1 n2) uint8 sampled-bin indicator in the same
  * layout; wlist (nw) the last occurrence of every distinct bin (linops.py:357); grids ncoils * D
  * complex64 workspace; y / ymeas (ncoils, ystride); partial: sr_cart3_partial_blocks(N, ncoils)
  * doubles of |A x - y|^2 when ymeas is given.  Epilogue coef/u/d as sr_cart_normal. */

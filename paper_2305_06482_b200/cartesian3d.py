@@ -5,8 +5,9 @@ Drop-in for the reference plugin ``_CartesianMaskKernel`` on a 3-D grid
 dimensionality; the 2-D K1/K2 kernels (cartesian.py) cover 1-D and 2-D grids.  The
 operator runs the per-axis grid pipeline of the gridded NUFFT (csrc/nufft.cu) with an
 oversampled grid equal to the image grid and unit apodisation: the embed places pixel r
-at index r mod n (the reference's ifftshift), every axis FFT leaves perm order, and
-the sample at centered bin f sits at sum_a perm(f_a mod n_a) * stride_a, so
+at index r mod n (the reference's ifftshift), the axis FFTs leave axes 0 and 1 in perm order
+and axis 2 in natural order, and the sample at centered bin f sits at
+perm(f_0) n_1 n_2 + perm(f_1) n_2 + f_2 (all mod n_a), so
 no centering phase is needed.  The normal op multiplies the spectrum by the sampled-bin
 indicator / D between the forward and the inverse passes.
 """
@@ -49,6 +50,9 @@ class Cartesian3DKernel:
         n0, n1, n2 = self.dims
         pos = []
         for a, n in enumerate(self.dims):
+            if a == 2:  # the grid pipeline keeps the contiguous axis in natural order
+                pos.append(np.mod(f[:, a], n))
+                continue
             pp = perm_positions(n) if n > 1 else np.zeros(1, dtype=np.int64)
             pos.append(pp[np.mod(f[:, a], n)])
         spos = (pos[0] * n1 * n2 + pos[1] * n2 + pos[2]).astype(np.int64)

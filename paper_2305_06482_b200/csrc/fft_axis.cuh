@@ -88,7 +88,7 @@ struct AxCfg {
 // contiguous rows of length N: fwd natural -> perm, inv perm -> natural (in place, unnormalised)
 template <int P, int Q>
 __global__ void __launch_bounds__(AxCfg<P, Q>::T)
-k_fft_rows(float2* __restrict__ data, long long nrows, int inv) {
+k_fft_rows(float2* __restrict__ data, long long nrows, int inv, int nat) {
   using S = FftShape<P, Q>;
   using A = AxCfg<P, Q>;
   constexpr int N = S::N, ROWS = A::ROWS, T = A::T;
@@ -124,14 +124,15 @@ k_fft_rows(float2* __restrict__ data, long long nrows, int inv) {
       }
       __syncthreads();
     }
+    // nat: the row leaves in natural frequency order (perm position of k read from shared memory)
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
-      base[e] = buf[l3 * S::VS + S::pad(pos)];
+      base[e] = buf[l3 * S::VS + S::pad(nat ? S::perm_pos(pos) : pos)];
     }
   } else {
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
-      buf[l3 * S::VS + S::pad(pos)] = base[e];
+      buf[l3 * S::VS + S::pad(nat ? S::perm_pos(pos) : pos)] = base[e];
     }
     __syncthreads();
     if (P > 1) {
@@ -248,7 +249,7 @@ k_fft_strided(float2* __restrict__ data, long long inner, int inv, AxPrune pr, i
 }
 
 template <int P, int Q>
-int launch_rows(float2* data, long long nrows, int inv, cudaStream_t st) {
+int launch_rows(float2* data, long long nrows, int inv, cudaStream_t st, int nat = 0) {
   using A = AxCfg<P, Q>;
   using S = FftShape<P, Q>;
   const size_t smem = sizeof(float2) * (S::N + A::ROWS * S::VS);
@@ -260,7 +261,7 @@ int launch_rows(float2* data, long long nrows, int inv, cudaStream_t st) {
   }
   const long long nb = (nrows + A::ROWS - 1) / A::ROWS;
   if (nb > 0x7fffffffLL) return SR_EINVAL;
-  k_fft_rows<P, Q><<<(unsigned)nb, A::T, smem, st>>>(data, nrows, inv);
+  k_fft_rows<P, Q><<<(unsigned)nb, A::T, smem, st>>>(data, nrows, inv, nat);
   SR_CHECK_LAUNCH();
   return SR_OK;
 }
@@ -369,10 +370,12 @@ k_embed_rows(const RowGeom rg) {
     }
     __syncthreads();
   }
+  // the grid row is stored in natural frequency order along axis 2 (contiguous tile rows for the
+  // gridding's bulk copies); the strided axes stay in perm order
   const int nv = (int)min((long long)ROWS, nrows - row0);
   for (int e = tid; e < nv * N; e += T) {
     const int l3 = e / N, pos = e - l3 * N;
-    rg.grid[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(pos)];
+    rg.grid[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(S::perm_pos(pos))];
   }
 }
 
@@ -417,7 +420,7 @@ k_rows_crop(const RowGeom rg) {
     float2* dst = bufs + (j & 1) * TILE;
     for (int e = tid; e < nv * N; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
-      cp_async8(dst + l3 * S::VS + S::pad(pos), gj + rbase[l3] + pos);
+      cp_async8(dst + l3 * S::VS + S::pad(S::perm_pos(pos)), gj + rbase[l3] + pos);  // natural along axis 2
     }
     cp_async_commit();
   };

@@ -23,6 +23,16 @@ int SR_CAT(sr_fft_axis_b, SR_BUCKET_ID)(float2* data, long long outer, int n, lo
   }
 }
 
+// contiguous rows whose frequency side is in natural order (grid rows of the NUFFT pipeline)
+int SR_CAT(sr_fft_rows_nat_b, SR_BUCKET_ID)(float2* data, long long nrows, int n, int inv, cudaStream_t st) {
+  switch (n) {
+#define X(N_, P_, Q_) case N_: return launch_rows<P_, Q_>(data, nrows, inv, st, 1);
+    SR_BUCKET_SIZES(X)
+#undef X
+    default: return SR_EUNSUPPORTED;
+  }
+}
+
 int SR_CAT(sr_fft_axis_pruned_b, SR_BUCKET_ID)(float2* data, long long outer, int n, long long inner, int inv,
                                               AxPrune pr, cudaStream_t st) {
   switch (n) {
