@@ -357,25 +357,29 @@ k_embed_rows(const RowGeom rg) {
 #pragma unroll
   for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
   __syncthreads();
+  // Step 2 writes straight from registers: the grid row is stored in natural frequency order
+  // along axis 2 (a gridding tile row is one contiguous run), frequency k2 + Q k1 of group k2 --
+  // lanes run over k2, so each k1 is a coalesced run of Q consecutive cells.  The strided axes
+  // stay in perm order.
+  const int nv = (int)min((long long)ROWS, nrows - row0);
   if (P > 1) {
     for (int it = tid; it < ROWS * Q; it += T) {
       const int l2 = it / Q, k2 = it - l2 * Q;
+      if (l2 >= nv) continue;
       float2 g[P];
-      float2* gp = buf + l2 * S::VS + S::GS * k2;
+      const float2* gp = buf + l2 * S::VS + S::GS * k2;
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
       fft_s2_fwd<P>(g);
+      float2* gr = rg.grid + rbase[l2] + k2;
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      for (int k1 = 0; k1 < P; ++k1) gr[Q * k1] = g[k1];
     }
-    __syncthreads();
-  }
-  // the grid row is stored in natural frequency order along axis 2 (contiguous tile rows for the
-  // gridding's bulk copies); the strided axes stay in perm order
-  const int nv = (int)min((long long)ROWS, nrows - row0);
-  for (int e = tid; e < nv * N; e += T) {
-    const int l3 = e / N, pos = e - l3 * N;
-    rg.grid[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(S::perm_pos(pos))];
+  } else {
+    for (int e = tid; e < nv * N; e += T) {
+      const int l3 = e / N, pos = e - l3 * N;
+      rg.grid[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(pos)];
+    }
   }
 }
 
