@@ -419,12 +419,24 @@ k_rows_crop(const RowGeom rg) {
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = make_float2(0.f, 0.f);
   __syncthreads();  // rbase
+  // Grid rows are natural-order along axis 2.  With Q <= P (one step-2' task per thread) the row
+  // lands in shared memory as it is (contiguous 16-byte cp.async), step 2' reads its group at the
+  // natural positions k2 + Q k1 (lanes over k2: conflict-free) and, after a barrier, writes the
+  // perm-padded layout step 1' expects; otherwise each cell goes straight to its perm position.
+  constexpr bool NATLOAD = (Q <= P) && (N % 2 == 0) && (S::VS % 2 == 0);
   auto issue = [&](int j) {
     const float2* gj = rg.grid + (long long)j * rg.G;
     float2* dst = bufs + (j & 1) * TILE;
-    for (int e = tid; e < nv * N; e += T) {
-      const int l3 = e / N, pos = e - l3 * N;
-      cp_async8(dst + l3 * S::VS + S::pad(S::perm_pos(pos)), gj + rbase[l3] + pos);  // natural along axis 2
+    if constexpr (NATLOAD) {
+      for (int e = 2 * tid; e < nv * N; e += 2 * T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        cp_async16(dst + l3 * S::VS + pos, gj + rbase[l3] + pos);
+      }
+    } else {
+      for (int e = tid; e < nv * N; e += T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        cp_async8(dst + l3 * S::VS + S::pad(S::perm_pos(pos)), gj + rbase[l3] + pos);
+      }
     }
     cp_async_commit();
   };
@@ -442,7 +454,24 @@ k_rows_crop(const RowGeom rg) {
     for (int q = 0; q < Q; ++q) m[q] = (i2s[q] >= 0) ? mj[i2s[q]] : make_float2(0.f, 0.f);
     __syncthreads();
     float2* buf = bufs + (j & 1) * TILE;
-    if (P > 1) {
+    if constexpr (NATLOAD && P > 1) {
+      const bool has = tid < ROWS * Q;
+      const int l2 = tid / Q, k2 = tid - l2 * Q;
+      float2 g[P];
+      if (has) {
+        const float2* gn = buf + l2 * S::VS + k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = gn[Q * k1];
+        fft_s2_inv<P, Q>(g, k2, tw);
+      }
+      __syncthreads();  // every natural-order read done before the perm-order writes
+      if (has) {
+        float2* gp = buf + l2 * S::VS + S::GS * k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      }
+      __syncthreads();
+    } else if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
         const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
