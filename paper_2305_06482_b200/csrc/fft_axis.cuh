@@ -130,12 +130,33 @@ k_fft_rows(float2* __restrict__ data, long long nrows, int inv, int nat) {
       base[e] = buf[l3 * S::VS + S::pad(nat ? S::perm_pos(pos) : pos)];
     }
   } else {
+    // nat (natural-order frequency rows, Q <= P): the row is staged as it is, step 2' reads its
+    // group at the natural positions k2 + Q k1 and writes the perm layout after a barrier
+    constexpr bool NATOK = (Q <= P) && (P > 1);
+    const bool natload = NATOK && nat;
     for (int e = tid; e < nvalid; e += T) {
       const int l3 = e / N, pos = e - l3 * N;
-      buf[l3 * S::VS + S::pad(nat ? S::perm_pos(pos) : pos)] = base[e];
+      buf[l3 * S::VS + (natload ? pos : S::pad(nat ? S::perm_pos(pos) : pos))] = base[e];
     }
     __syncthreads();
-    if (P > 1) {
+    if (natload) {
+      const bool has = tid < ROWS * Q;
+      const int l2 = tid / Q, k2 = tid - l2 * Q;
+      float2 g[P];
+      if (has) {
+        const float2* gn = buf + l2 * S::VS + k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = gn[Q * k1];
+        fft_s2_inv<P, Q>(g, k2, tw);
+      }
+      __syncthreads();
+      if (has) {
+        float2* gp = buf + l2 * S::VS + S::GS * k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) gp[k1] = g[k1];
+      }
+      __syncthreads();
+    } else if (P > 1) {
       for (int it = tid; it < ROWS * Q; it += T) {
         const int l2 = it / Q, k2 = it - l2 * Q;
         float2 g[P];
