@@ -191,129 +191,6 @@ k_wav_syn2(const float2* __restrict__ coef, float2* __restrict__ out, int h, int
   }
 }
 
-// ------------------------------------------------------- coarse levels in one CTA
-// Levels l0..L-1 of the 2-D prox (analysis with the soft threshold, then synthesis) on the
-// (h0 x w0) low-pass corner of `buf` (row stride ld), in place, one CTA per slice: the corner and
-// its subbands live in shared memory, so the ~4 launches of those small levels become one.  Every
-// output is the same sequence of fmaf as k_wav_ana2 / k_wav_syn2 computes (bitwise equal).
-constexpr int CO_THREADS = 1024;
-
-__device__ __forceinline__ void co_ana(const float2* in, float2* out, float2* tlo, float2* thi, int h, int w,
-                                       int ld, float t, bool last) {
-  const int hh = h >> 1, hw = w >> 1;
-  for (int e = threadIdx.x; e < h * hw; e += CO_THREADS) {
-    const int r = e / hw, j = e - r * hw;
-    float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float2 v = in[r * ld + wrap(2 * j + k, w)];
-      lo.x = fmaf(c_lo[k], v.x, lo.x); lo.y = fmaf(c_lo[k], v.y, lo.y);
-      hi.x = fmaf(c_hi[k], v.x, hi.x); hi.y = fmaf(c_hi[k], v.y, hi.y);
-    }
-    tlo[r * hw + j] = lo;
-    thi[r * hw + j] = hi;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < hh * hw; e += CO_THREADS) {
-    const int i = e / hw, j = e - i * hw;
-    float2 ll = make_float2(0.f, 0.f), lh = ll, hl = ll, hh2 = ll;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int r = wrap(2 * i + k, h);
-      const float2 a = tlo[r * hw + j], c = thi[r * hw + j];
-      ll.x = fmaf(c_lo[k], a.x, ll.x); ll.y = fmaf(c_lo[k], a.y, ll.y);
-      hl.x = fmaf(c_hi[k], a.x, hl.x); hl.y = fmaf(c_hi[k], a.y, hl.y);
-      lh.x = fmaf(c_lo[k], c.x, lh.x); lh.y = fmaf(c_lo[k], c.y, lh.y);
-      hh2.x = fmaf(c_hi[k], c.x, hh2.x); hh2.y = fmaf(c_hi[k], c.y, hh2.y);
-    }
-    if (t >= 0.f) {
-      lh = soft(lh, t); hl = soft(hl, t); hh2 = soft(hh2, t);
-      if (last) ll = soft(ll, t);
-    }
-    out[i * ld + j] = ll;
-    out[i * ld + hw + j] = lh;
-    out[(hh + i) * ld + j] = hl;
-    out[(hh + i) * ld + hw + j] = hh2;
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void co_syn(const float2* cf, float2* out, float2* ulo, float2* uhi, int h, int w,
-                                       int ld) {
-  const int hh = h >> 1, hw = w >> 1;
-  for (int e = threadIdx.x; e < hh * w; e += CO_THREADS) {
-    const int r = e / w, n = e - r * w;
-    const int par = n & 1;
-    float2 a = make_float2(0.f, 0.f), c = a;
-#pragma unroll
-    for (int tt = 0; tt < 4; ++tt) {
-      const int k = par + 2 * tt;
-      const int jj = wrap((n - k) / 2, hw);
-      const float fl = c_lo[k], fh = c_hi[k];
-      const float2 ll = cf[r * ld + jj], lh = cf[r * ld + hw + jj];
-      const float2 hl = cf[(hh + r) * ld + jj], h2 = cf[(hh + r) * ld + hw + jj];
-      a.x = fmaf(fl, ll.x, fmaf(fh, lh.x, a.x)); a.y = fmaf(fl, ll.y, fmaf(fh, lh.y, a.y));
-      c.x = fmaf(fl, hl.x, fmaf(fh, h2.x, c.x)); c.y = fmaf(fl, hl.y, fmaf(fh, h2.y, c.y));
-    }
-    ulo[r * w + n] = a;
-    uhi[r * w + n] = c;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < h * w; e += CO_THREADS) {
-    const int m = e / w, n = e - m * w;
-    const int par = m & 1;
-    float2 v = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int tt = 0; tt < 4; ++tt) {
-      const int k = par + 2 * tt;
-      const int ii = wrap((m - k) / 2, hh);
-      const float2 a = ulo[ii * w + n], c = uhi[ii * w + n];
-      v.x = fmaf(c_lo[k], a.x, fmaf(c_hi[k], c.x, v.x));
-      v.y = fmaf(c_lo[k], a.y, fmaf(c_hi[k], c.y, v.y));
-    }
-    out[m * ld + n] = v;
-  }
-  __syncthreads();
-}
-
-// smem: A (h0 x w0 corner / synthesis target), B (subbands of the level being analysed), T (the
-// row-pass temporaries: 2 x h0 x w0 / 2)
-__global__ void __launch_bounds__(CO_THREADS)
-k_wav_coarse2(float2* __restrict__ buf, int h0, int w0, int ld, long long bs, int nlev,
-              const float* __restrict__ thresh, float hthresh) {
-  extern __shared__ __align__(16) float2 co_sm[];
-  float2* A = co_sm;
-  float2* B = A + h0 * w0;
-  float2* T = B + h0 * w0;
-  float2* g = buf + blockIdx.x * bs;
-  const float t = thresh ? thresh[blockIdx.x] : hthresh;
-  for (int e = threadIdx.x; e < h0 * w0; e += CO_THREADS) {
-    const int r = e / w0, c = e - r * w0;
-    A[e] = g[(long long)r * ld + c];
-  }
-  __syncthreads();
-  // analysis: level k reads the corner of (k even ? A : B) and writes (k even ? B : A)
-  for (int k = 0; k < nlev; ++k) {
-    const int h = h0 >> k, w = w0 >> k;
-    const float2* src = (k & 1) ? B : A;
-    float2* dst = (k & 1) ? A : B;
-    co_ana(src, dst, T, T + (h * w) / 2, h, w, w0, t, k == nlev - 1);
-  }
-  // synthesis: level k reads (k even ? B : A) and writes the corner it was analysed from
-  for (int k = nlev - 1; k >= 0; --k) {
-    const int h = h0 >> k, w = w0 >> k;
-    const float2* cf = (k & 1) ? A : B;
-    float2* dst = (k & 1) ? B : A;
-    co_syn(cf, dst, T, T + (h / 2) * w, h, w, w0);
-  }
-  for (int e = threadIdx.x; e < h0 * w0; e += CO_THREADS) {
-    const int r = e / w0, c = e - r * w0;
-    g[(long long)r * ld + c] = A[e];
-  }
-}
-
-inline size_t coarse_smem(int h0, int w0) { return sizeof(float2) * 3 * (size_t)h0 * w0; }
-
 }  // namespace
 
 extern "C" {
@@ -361,37 +238,6 @@ int sr_wavelet_prox2(const sr_c64* v, sr_c64* out, sr_c64* buf0, sr_c64* buf1, i
                      float beta, void* stream) {
   if (levels < 1 || levels > 8 || !v || !out || !buf0 || !buf1) return SR_EINVAL;
   sr_c64* bufs[2] = {buf0, buf1};
-  // levels >= l0 = 2 in one CTA per slice when their corner fits shared memory (~4 launches on
-  // tiny grids -> one)
-  const int l0 = 2;
-  if (levels >= l0 + 2 && coarse_smem(ny >> l0, nx >> l0) <= 200 * 1024) {
-    const sr_c64* src = v;
-    for (int l = 0; l < l0; ++l) {
-      const int rc = sr_wavelet_ana2(src, bufs[l % 2], ny >> l, nx >> l, nx, bs, batch, thresh, hthresh, 0,
-                                     nullptr, stream);
-      if (rc) return rc;
-      src = bufs[l % 2];
-    }
-    static int configured = 0;
-    const size_t smem = coarse_smem(ny >> l0, nx >> l0);
-    if ((size_t)configured < smem) {
-      if (cudaFuncSetAttribute(k_wav_coarse2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return SR_ECUDA;
-      configured = (int)smem;
-    }
-    k_wav_coarse2<<<batch, CO_THREADS, smem, (cudaStream_t)stream>>>((float2*)bufs[(l0 - 1) % 2], ny >> l0,
-                                                                       nx >> l0, nx, bs, levels - l0, thresh,
-                                                                       thresh ? -1.f : hthresh);
-    SR_CHECK_LAUNCH();
-    for (int l = l0 - 1; l >= 0; --l) {
-      sr_c64* dst = (l == 0) ? out : bufs[(l - 1) % 2];
-      const int rc = (l == 0) ? sr_wavelet_syn2(bufs[0], dst, ny, nx, nx, bs, batch, zout, xold, beta, stream)
-                              : sr_wavelet_syn2(bufs[l % 2], dst, ny >> l, nx >> l, nx, bs, batch, nullptr, nullptr,
-                                                0.f, stream);
-      if (rc) return rc;
-    }
-    return SR_OK;
-  }
   const sr_c64* src = v;
   for (int l = 0; l < levels; ++l) {
     const int rc = sr_wavelet_ana2(src, bufs[l % 2], ny >> l, nx >> l, nx, bs, batch, thresh, hthresh,

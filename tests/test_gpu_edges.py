@@ -248,40 +248,3 @@ def test_c_abi_plans_reject_out_of_range_coordinates(cuda):
     _lib.call("sr_nufft_plan_create", pts.ctypes.data, 2, 2, cdims, 2.0, 4, 0, ctypes.byref(nplan), dv.stream())
     _lib.call("sr_nufft_plan_destroy", nplan)
 
-
-@pytest.mark.parametrize("dims,levels,B", [((256, 256), 4, 2), ((320, 320), 4, 1), ((256, 160), 5, 3),
-                                           ((64, 64), 3, 1)])
-def test_wavelet_prox_coarse_levels_bitwise(cuda, dims, levels, B):
-    """sr_wavelet_prox2 runs levels >= 2 in one CTA per slice (k_wav_coarse2) when the corner fits
-    shared memory: bitwise equal to the level-by-level launches (same fmaf sequence), with the
-    device threshold, the FISTA momentum epilogue, and without a threshold."""
-    from paper_2305_06482_b200 import _device as dv
-    from paper_2305_06482_b200 import _lib
-    ny, nx = dims
-    D = ny * nx
-    g = torch.Generator("cuda").manual_seed(5)
-    v = torch.randn(B, D, dtype=torch.complex64, device="cuda", generator=g)
-    xold = torch.randn(B, D, dtype=torch.complex64, device="cuda", generator=g)
-    thresh = torch.linspace(0.05, 0.3, B, device="cuda", dtype=torch.float32)
-    st = dv.stream()
-    for th in (thresh, None):
-        outs = []
-        for fused in (True, False):
-            b0, b1 = torch.zeros_like(v), torch.zeros_like(v)
-            out, z = torch.empty_like(v), torch.empty_like(v)
-            if fused:
-                _lib.call("sr_wavelet_prox2", dv.ptr(v), dv.ptr(out), dv.ptr(b0), dv.ptr(b1), ny, nx, D, B, levels,
-                          dv.ptr(th), -1.0, dv.ptr(z), dv.ptr(xold), 0.37, st)
-            else:
-                bufs, src = (b0, b1), v
-                for lv in range(levels):
-                    _lib.call("sr_wavelet_ana2", dv.ptr(src), dv.ptr(bufs[lv % 2]), ny >> lv, nx >> lv, nx, D, B,
-                              dv.ptr(th), -1.0, int(lv == levels - 1), None, st)
-                    src = bufs[lv % 2]
-                for lv in range(levels - 1, -1, -1):
-                    dst = out if lv == 0 else bufs[(lv - 1) % 2]
-                    _lib.call("sr_wavelet_syn2", dv.ptr(bufs[lv % 2]), dv.ptr(dst), ny >> lv, nx >> lv, nx, D, B,
-                              dv.ptr(z) if lv == 0 else None, dv.ptr(xold) if lv == 0 else None,
-                              0.37 if lv == 0 else 0.0, st)
-            outs.append((out, z))
-        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
