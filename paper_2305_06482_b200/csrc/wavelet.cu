@@ -37,6 +37,11 @@ __device__ __forceinline__ float2 soft(float2 v, float t) {
 }
 
 __device__ __forceinline__ int wrap(int i, int n) {
+  // periodic index; the tiles reach at most one period past either edge except on the smallest
+  // levels, so the integer division is off the common path
+  if ((unsigned)i < (unsigned)n) return i;
+  if (i >= n && i < 2 * n) return i - n;
+  if (i < 0 && i >= -n) return i + n;
   i %= n;
   return i < 0 ? i + n : i;
 }
