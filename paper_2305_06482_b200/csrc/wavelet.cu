@@ -63,9 +63,19 @@ k_wav_ana2(const float2* __restrict__ src, float2* __restrict__ dst, int h, int 
   const float2* s = src + b * bs;
   float2* o = dst + b * bs;
   const int tid = threadIdx.y * TJ + threadIdx.x;
-  for (int e = tid; e < AR * AC; e += 256) {
-    const int r = e / AC, c = e - r * AC;
-    tin[r][c] = s[(long long)wrap(2 * i0 + r, h) * ld + wrap(2 * j0 + c, w)];
+  if (2 * i0 + AR <= h && 2 * j0 + AC <= w && !(ld & 1) && !(reinterpret_cast<size_t>(s) & 15)) {
+    // interior tile: no wrap, two pixels per 16-byte load (even column start and row stride)
+    for (int e = tid; e < AR * (AC / 2); e += 256) {
+      const int r = e / (AC / 2), c = 2 * (e - r * (AC / 2));
+      const float4 v = *reinterpret_cast<const float4*>(s + (long long)(2 * i0 + r) * ld + 2 * j0 + c);
+      tin[r][c] = make_float2(v.x, v.y);
+      tin[r][c + 1] = make_float2(v.z, v.w);
+    }
+  } else {
+    for (int e = tid; e < AR * AC; e += 256) {
+      const int r = e / AC, c = e - r * AC;
+      tin[r][c] = s[(long long)wrap(2 * i0 + r, h) * ld + wrap(2 * j0 + c, w)];
+    }
   }
   __syncthreads();
   for (int e = tid; e < AR * TJ; e += 256) {
@@ -144,11 +154,12 @@ k_wav_syn2(const float2* __restrict__ coef, float2* __restrict__ out, int h, int
   const int ci0 = m0 / 2 - 3, cj0 = n0 / 2 - 3;
   const float2* cb = coef + b * bs;
   const int tid = threadIdx.x;
+  const bool interior = ci0 >= 0 && ci0 + SR_ <= hh && cj0 >= 0 && cj0 + SC_ <= hw;
   for (int e = tid; e < 4 * SR_ * SC_; e += 256) {
     const int qd = e / (SR_ * SC_);
     const int rem = e - qd * SR_ * SC_;
     const int r = rem / SC_, c = rem - r * SC_;
-    const int gi = wrap(ci0 + r, hh), gj = wrap(cj0 + c, hw);
+    const int gi = interior ? ci0 + r : wrap(ci0 + r, hh), gj = interior ? cj0 + c : wrap(cj0 + c, hw);
     const int oi = (qd & 2) ? hh : 0, oj = (qd & 1) ? hw : 0;
     q[qd][r][c] = cb[(long long)(oi + gi) * ld + oj + gj];
   }
