@@ -166,8 +166,19 @@ def slice_compression(y: torch.Tensor, keep: int, valid_n=None, threads: int | N
         return u[:, :keep].conj().T
 
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, ncpu))) as ex:
-        return np.stack(list(ex.map(one, range(S))))
+    # one BLAS thread per worker: a multi-threaded BLAS inside every worker oversubscribes the host
+    # (the compression step varied 38-140 ms between runs)
+    try:
+        from threadpoolctl import threadpool_limits
+        limit = threadpool_limits(limits=1)
+    except ImportError:  # pragma: no cover - threadpoolctl ships with the image
+        limit = None
+    try:
+        with cf.ThreadPoolExecutor(max_workers=threads or max(1, min(S, ncpu))) as ex:
+            return np.stack(list(ex.map(one, range(S))))
+    finally:
+        if limit is not None:
+            limit.restore_original_limits()
 
 
 def compress_slices(maps: torch.Tensor, y: torch.Tensor, keep: int, valid_n=None, comp=None):
