@@ -66,7 +66,8 @@ class CartesianKernel:
             g_idx, g_ptr, s_idx, s_ptr = [], [], [], []
             g_base = s_base = 0
             for p in per_slice:
-                blk = (p.spos.astype(np.int64) % self.nx) // cb
+                # small block ids (uint16): numpy's stable sort is a radix sort for them
+                blk = ((p.spos.astype(np.int64) % self.nx) // cb).astype(np.uint16)
                 order = np.argsort(blk, kind="stable").astype(np.int32)
                 g_idx.append(order)
                 g_ptr.append(g_base + np.r_[0, np.cumsum(np.bincount(blk, minlength=self.nblk))])

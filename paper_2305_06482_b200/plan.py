@@ -78,10 +78,13 @@ def cartesian_plan(dims: tuple[int, ...], points: np.ndarray) -> CartesianPlan:
     ph = np.exp(1j * ang).astype(np.complex64)
     maskT = np.zeros(nx * ny, dtype=np.uint8)
     maskT[pos_x * ny + pos_y] = 1
-    # last occurrence of every distinct bin
-    rev = spos[::-1]
-    _, first_in_rev = np.unique(rev, return_index=True)
-    wlist = np.sort(len(spos) - 1 - first_in_rev).astype(np.int32)
+    # last occurrence of every distinct bin: a stable sort by bin (radix sort on int32) keeps the
+    # samples of a bin in trajectory order, so the last of each run is the last occurrence
+    order = np.argsort(spos, kind="stable").astype(np.int32)
+    s = spos[order]
+    last = np.ones(len(s), dtype=bool)
+    last[:-1] = s[1:] != s[:-1]
+    wlist = np.sort(order[last], kind="stable").astype(np.int32)
     return CartesianPlan(ny, nx, int(pts.shape[0]), spos, ph, maskT, wlist)
 
 
