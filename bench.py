@@ -282,7 +282,8 @@ def run_extras(rank: int, world: int, dev) -> dict:
 
     * recon.config0: full config-0 coil-sketched reconstruction (256^2, 16 -> 4+4, 10 x 10 FISTA)
       through the default drop-in API, median of 3 (CUDA events), with the CPU oracle's wall
-      time and the NRMSE against it (rank 0 only; a replica config);
+      time and the NRMSE against it (rank 0 only; a replica config); recon.config3: the config-3
+      radial NUFFT reconstruction, GPU wall only;
     * sharded.config2: the 256 readout-decoupled slices of config 2 split over the N ranks (strong
       scaling, no data-path collective): recon wall (max over ranks) and slices/s, at N = 1 with
       two slices checked against the oracle and a 16-slice oracle process pool timed beside it;
@@ -300,6 +301,12 @@ def run_extras(rank: int, world: int, dev) -> dict:
                                                       "expected_counts", "cpu_oracle_wall_s", "cpu_cores",
                                                       "nrmse_vs_oracle", "rel_l2_vs_oracle", "speedup")}
         out["recon"]["config0"]["unit"] = "s"
+        # config 3 (2-D golden-angle radial NUFFT recon): GPU wall only (its oracle takes ~80 s;
+        # parity: tests/test_gpu_configs.py, profiles/r02c_configs.jsonl)
+        r3 = bc.run_2d(3, False)
+        out["recon"]["config3"] = {k: r3[k] for k in ("what", "gpu_wall_s", "gpu_wall_s_runs", "counts",
+                                                      "expected_counts")}
+        out["recon"]["config3"]["unit"] = "s"
     torch.cuda.empty_cache()
     r2 = bc.run_cfg2(rank == 0 and world == 1, 256, 16 if world == 1 else 0)
     torch.cuda.empty_cache()
@@ -310,6 +317,13 @@ def run_extras(rank: int, world: int, dev) -> dict:
         out["recon"]["config2_wall_s"] = r2["gpu_wall_s"]
         out["sharded"]["config4"] = {k: r4[k] for k in ("what", "n_gpus", "scaling", "sketched_normal_apply_s",
                                                         "plan_build_s", "data")}
+        # SURVEY 8(d)'s diagnostic streaming model of the sketched NUFFT normal op (the oversampled
+        # grids through every FFT pass): 40.7 GB per apply at the measured HBM peak
+        peak, _ = measured_peak()
+        model_s = 40.7e9 / (peak * 1e9)
+        out["sharded"]["config4"]["streaming_model"] = {
+            "bytes": 40.7e9, "ms_at_peak": model_s * 1e3,
+            "frac": model_s / world / r4["sketched_normal_apply_s"] if r4["sketched_normal_apply_s"] else None}
         if world > 1:
             import torch.distributed as dist
             out["sharded"]["config4"]["collective"] = (f"{dist.get_backend()} all-reduce (sum) of the 83.9 MB "
