@@ -10,7 +10,9 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_native" / "libsketchrecon_b200.so"
+# SR_LIB_PATH: an alternative build of the same library (A/B measurements of a kernel change in
+# one process's box session, tools only); unset -> the in-tree build
+LIB_PATH = Path(os.environ.get("SR_LIB_PATH") or Path(__file__).resolve().parent / "_native" / "libsketchrecon_b200.so")
 
 _vp = C.c_void_p
 _i = C.c_int
