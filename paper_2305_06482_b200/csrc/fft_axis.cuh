@@ -10,6 +10,9 @@
 #ifndef SR_CROP_MINB
 #define SR_CROP_MINB 1
 #endif
+#ifndef SR_EMBED_LOOP_MINB
+#define SR_EMBED_LOOP_MINB 1
+#endif
 
 // Zero-padding structure of an oversampled NUFFT axis of length g holding an image axis of
 // length n (centered: image index i sits at grid index (i - n/2) mod g, linops.py:438-446).
@@ -404,6 +407,88 @@ k_embed_rows(const RowGeom rg) {
   }
 }
 
+// The same pass with the coils looped inside the CTA (enough image rows to fill the GPU, short
+// rows): a CTA owns ROWS image rows, keeps (x - a) / apod of its pixels in registers and streams the
+// coil maps through them, the next coil's map values in flight (registers) while the current coil
+// transforms -- the one-shot kernel above lives on load latency (config 4: 41 % of the DRAM peak).
+template <int P, int Q>
+__global__ void __launch_bounds__(AxCfg<P, Q>::T, SR_EMBED_LOOP_MINB)
+k_embed_rows_loop(const RowGeom rg) {
+  using S = FftShape<P, Q>;
+  using A = AxCfg<P, Q>;
+  constexpr int N = S::N, ROWS = A::ROWS, T = A::T;
+  extern __shared__ __align__(16) float2 dsm[];
+  __shared__ long long rbase[ROWS];
+  float2* tw = dsm;
+  float2* buf = dsm + N;
+  const int tid = threadIdx.x;
+  const long long nrows = (long long)rg.n0 * rg.n1;  // image rows
+  const long long row0 = (long long)blockIdx.x * ROWS;
+  const int lr = tid / P, p = tid % P;
+  init_tw_s1<P, Q>(tw, tid, T);
+  const long long rid = row0 + lr;
+  const bool valid = rid < nrows;
+  const int i0 = valid ? (int)(rid / rg.n1) : 0, i1 = valid ? (int)(rid - (long long)i0 * rg.n1) : 0;
+  if (p == 0) rbase[lr] = ((long long)ax_wrap(i0, rg.n0, rg.g0) * rg.g1 + ax_wrap(i1, rg.n1, rg.g1)) * N;
+  const long long pixrow = ((long long)i0 * rg.n1 + i1) * rg.n2;
+  const float s01 = valid ? rg.ia0[i0] * rg.ia1[i1] : 0.f;
+  const int h2 = rg.n2 >> 1;
+  // pixel of each of the thread's positions k2 = p + P q (clamped to a valid address outside the
+  // image, where the scaled input is zero)
+  int i2s[Q];
+  float2 xs[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int k2 = p + P * q;
+    const bool in = valid && ax_inside(k2, rg.n2, N);
+    i2s[q] = in ? ((k2 < rg.n2 - h2) ? k2 + h2 : k2 - N + h2) : 0;
+    float2 xv = rg.x[pixrow + i2s[q]];
+    if (rg.anchor) xv = csub(xv, rg.anchor[pixrow + i2s[q]]);
+    xs[q] = in ? cscale(xv, s01 * rg.ia2[i2s[q]]) : make_float2(0.f, 0.f);
+  }
+  const float2* mp = rg.maps + pixrow;
+  float2 mv[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) mv[q] = mp[i2s[q]];
+  const int nv = (int)min((long long)ROWS, nrows - row0);
+  __syncthreads();  // tw, rbase
+  for (int j = 0; j < rg.ncoils; ++j) {
+    float2 r[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) r[q] = cmul(mv[q], xs[q]);
+    if (j + 1 < rg.ncoils) {
+      const float2* mn = mp + (long long)(j + 1) * rg.D;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) mv[q] = mn[i2s[q]];
+    }
+    fft_s1_fwd<P, Q>(r, p, tw);
+#pragma unroll
+    for (int k2 = 0; k2 < Q; ++k2) buf[lr * S::VS + S::GS * k2 + p] = r[k2];
+    __syncthreads();
+    float2* gj = rg.grid + (long long)j * rg.G;
+    if (P > 1) {
+      for (int it = tid; it < ROWS * Q; it += T) {
+        const int l2 = it / Q, k2 = it - l2 * Q;
+        if (l2 >= nv) continue;
+        float2 g[P];
+        const float2* gp = buf + l2 * S::VS + S::GS * k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) g[k1] = gp[k1];
+        fft_s2_fwd<P>(g);
+        float2* gr = gj + rbase[l2] + k2;
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) gr[Q * k1] = g[k1];
+      }
+    } else {
+      for (int e = tid; e < nv * N; e += T) {
+        const int l3 = e / N, pos = e - l3 * N;
+        gj[rbase[l3] + pos] = buf[l3 * S::VS + S::pad(pos)];
+      }
+    }
+    __syncthreads();  // buf is rewritten by the next coil
+  }
+}
+
 template <int P, int Q>
 __global__ void __launch_bounds__(AxCfg<P, Q>::T, SR_CROP_MINB)
 k_rows_crop(const RowGeom rg) {
@@ -542,6 +627,23 @@ int launch_row_fused(const RowGeom& rg, cudaStream_t st) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SR_ECUDA;
     cfg = true;
+  }
+  if constexpr (!INV && Q <= 16) {
+    // coil-looped embed: several coils and enough image rows for >= 2 CTAs per SM
+    const long long nimg = (long long)rg.n0 * rg.n1;
+    const long long nb = (nimg + A::ROWS - 1) / A::ROWS;
+    if (rg.ncoils >= 2 && nb >= 2 * 148 && nb <= 0x7fffffffLL) {
+      static bool cfg2 = false;
+      if (!cfg2) {
+        if (cudaFuncSetAttribute(k_embed_rows_loop<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+          return SR_ECUDA;
+        cfg2 = true;
+      }
+      k_embed_rows_loop<P, Q><<<(unsigned)nb, A::T, smem, st>>>(rg);
+      SR_CHECK_LAUNCH();
+      return SR_OK;
+    }
   }
   const int nplanes = INV ? (rg.i0b < 0 ? rg.n0 : rg.i0b) - rg.i0a : rg.n0;
   const long long nrows = INV ? (long long)nplanes * rg.n1 : (long long)rg.ncoils * rg.n0 * rg.n1;
