@@ -251,6 +251,19 @@ int sr_nufft_normal(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, i
                     const float* frac, const float* wgt, long long nsamples, sr_c64* out,
                     sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, const int* chunks,
                     int nchunks, int binsize, void* stream);
+/* sr_nufft_normal with the zeroing of the spread grid off the critical path (binned plans only,
+ * else SR_EUNSUPPORTED).  grids: 3 * ncoils * G complex64 -- the spectrum grids and two spread grids
+ * used in turn.  The call spreads into spread grid dst_index (0 | 1), which it zeroes first unless
+ * dst_clean != 0, and the gridding kernel zeroes the other one as it runs (that kernel leaves HBM
+ * nearly idle, so the stores are free).  A caller
+ * alternating dst_index may pass dst_clean = 1 from its second call on, as long as nothing else
+ * wrote the workspace in between.  Same result as sr_nufft_normal. */
+int sr_nufft_normal_pp(const sr_c64* x, const sr_c64* anchor, const sr_c64* maps, int ncoils,
+                       const int* dims, const int* gdims, const float* betas, int width,
+                       const float* ia0, const float* ia1, const float* ia2, const int* base,
+                       const float* frac, const float* wgt, long long nsamples, sr_c64* out,
+                       sr_c64* grids, const float* coef, const sr_c64* u, const sr_c64* d, const int* chunks,
+                       int nchunks, int binsize, int dst_index, int dst_clean, void* stream);
 /* sr_nufft_normal in two parts for the coil-sharded pipeline (config 4): _head runs the embed, the
  * forward passes, the gridding and the axis-0 inverse pass into `grids`; _tail finishes image
  * planes i0 in [i0a, i0b) only (remaining inverse passes, crop, conjugate coil sum, epilogue), so

@@ -59,6 +59,8 @@ SIGNATURES = {
     "sr_cart_tune_rows": [_i, _i],
     "sr_nufft_normal": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
                         _vp, _vp, _vp, _vp, _i, _i, _vp],
+    "sr_nufft_normal_pp": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp,
+                           _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "sr_nufft_normal_head": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _i,
                              _i, _vp],
     "sr_nufft_normal_tail": [_vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],

@@ -149,6 +149,7 @@ class GriddedKernel:
             ia.append(1.0 / kb_apodization(r / g, self.width, beta))
         self.ia = [dv.host_to_dev(v.astype(np.float32), torch.float32, dev) for v in ia]
         self._grids = None
+        self._pp = None  # (coil count, clean spread grid) of the ping-pong normal op
         self._wcache: dict = {}
         self.nparts = max(_lib.lib().sr_nufft_partial_blocks(self.n_points), self.nchunks)
 
@@ -247,10 +248,14 @@ class GriddedKernel:
         return base, frac, orig, chunks
 
     # ------------------------------------------------------------ helpers
-    def workspace(self, ncoils: int, batch: int | None = None, chunk: int = 0, normal: bool = True):
-        need = (2 if normal else 1) * ncoils * self.G
+    # spread grids of at least this many bytes are zeroed off the critical path (sr_nufft_normal_pp)
+    PP_MIN_BYTES = 1 << 28
+
+    def workspace(self, ncoils: int, batch: int | None = None, chunk: int = 0, normal: bool = True, slots: int = 2):
+        need = (slots if normal else 1) * ncoils * self.G
         if self._grids is None or self._grids.numel() < need:
             self._grids = torch.empty(need, dtype=torch.complex64, device=self.device)
+        self._pp = None  # whoever asked may write anywhere in the workspace
         return self._grids
 
     def _geom(self):
@@ -288,6 +293,19 @@ class GriddedKernel:
     # ------------------------------------------------------------ device API
     def normal(self, maps, x, out, *, anchor=None, coef=None, u=None, d=None, w=None, chunk=None):
         C = self._maps(maps)
+        if self.binned and 8 * C * self.G >= self.PP_MIN_BYTES and not torch.cuda.is_current_stream_capturing():
+            # large grids: two spread grids used in turn, the idle one zeroed while the gridding kernel
+            # runs (the state is the pair (coil count, clean spread grid); any other workspace user
+            # resets it)
+            pp = self._pp
+            grids = self.workspace(C, normal=True, slots=3)
+            idx, clean = (pp[1], 1) if pp is not None and pp[0] == C else (0, 0)
+            _lib.call("sr_nufft_normal_pp", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), C, *self._geom()[:4],
+                      *self._geom()[4:], dv.ptr(self.base), dv.ptr(self.frac), dv.ptr(self._weights(w, True)),
+                      self.n_points, dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), *self._bins(),
+                      idx, clean, dv.stream())
+            self._pp = (C, 1 - idx)
+            return out
         grids = self.workspace(C, normal=True)
         _lib.call("sr_nufft_normal", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), C, *self._geom()[:4],
                   *self._geom()[4:], dv.ptr(self.base), dv.ptr(self.frac), dv.ptr(self._weights(w, True)),

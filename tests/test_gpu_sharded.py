@@ -143,6 +143,46 @@ def test_nufft_normal_slabs_equal_normal(cuda):
         small.normal_slabs(m2, x2, torch.empty_like(x2), [(0, 10), (10, 20)], lambda lo, hi: None)
 
 
+def test_nufft_normal_pingpong_equals_normal(cuda):
+    """The normal op with two spread grids used in turn (the idle one zeroed on a library stream while
+    the gridding kernel runs, sr_nufft_normal_pp) == the one-grid normal op, over a run of calls with
+    other workspace users (forward / adjoint, another coil count, the slab pipeline) in between."""
+    kern, maps, x, _ = _slab_problem(cuda)
+    ref = torch.empty_like(x)
+    kern.normal(maps, x, ref)  # small grid: the plain path
+    assert kern._pp is None
+    x2 = torch.randn_like(x)
+    ref2 = torch.empty_like(x)
+    kern.normal(maps, x2, ref2)
+    kern.PP_MIN_BYTES = 0  # force the ping-pong path on this small grid
+    try:
+        def close(a, b):
+            return float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)) < 1e-6
+        out = torch.empty_like(x)
+        for k in range(5):
+            xin, want = (x, ref) if k % 2 == 0 else (x2, ref2)
+            out.fill_(float("nan"))
+            kern.normal(maps, xin, out)
+            assert kern._pp == (maps.shape[1], (k + 1) % 2)
+            assert close(out, want), k
+        # other users of the workspace reset the state; the next call zeroes its own grid
+        y = kern.forward(maps, x)
+        assert kern._pp is None
+        kern.adjoint(maps, y, torch.empty_like(x))
+        kern.normal(maps, x, out)
+        assert close(out, ref)
+        kern.normal(maps[:, :2].contiguous(), x, torch.empty_like(x))  # another coil count
+        kern.normal(maps, x2, out)
+        assert close(out, ref2)
+        n0 = SLAB_DIMS[0]
+        kern.normal_slabs(maps, x, torch.empty_like(x), [(0, n0 // 2), (n0 // 2, n0)], lambda lo, hi: None)
+        kern.normal(maps, x, out)
+        kern.normal(maps, x2, out)
+        assert close(out, ref2)
+    finally:
+        del kern.PP_MIN_BYTES  # back to the class default
+
+
 def _slab_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
