@@ -296,14 +296,15 @@ def run_extras(rank: int, world: int, dev) -> dict:
     import bench_configs as bc
     out = {"recon": {}, "sharded": {}}
     if rank == 0:
+        # config 3 (2-D golden-angle radial NUFFT recon): GPU wall only (its oracle takes ~80 s;
+        # parity: tests/test_gpu_configs.py, profiles/r02c_configs.jsonl); timed before config 0's
+        # CPU oracle runs in this process
+        r3 = bc.run_2d(3, False)
         r0 = bc.run_2d(0, True)
         out["recon"]["config0"] = {k: r0[k] for k in ("what", "gpu_wall_s", "gpu_wall_s_runs", "counts",
                                                       "expected_counts", "cpu_oracle_wall_s", "cpu_cores",
                                                       "nrmse_vs_oracle", "rel_l2_vs_oracle", "speedup")}
         out["recon"]["config0"]["unit"] = "s"
-        # config 3 (2-D golden-angle radial NUFFT recon): GPU wall only (its oracle takes ~80 s;
-        # parity: tests/test_gpu_configs.py, profiles/r02c_configs.jsonl)
-        r3 = bc.run_2d(3, False)
         out["recon"]["config3"] = {k: r3[k] for k in ("what", "gpu_wall_s", "gpu_wall_s_runs", "counts",
                                                       "expected_counts")}
         out["recon"]["config3"]["unit"] = "s"

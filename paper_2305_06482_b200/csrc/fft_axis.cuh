@@ -489,8 +489,10 @@ k_embed_rows_loop(const RowGeom rg) {
   }
 }
 
+// short rows (Q <= 12, config 4's 200-cell rows): capped at 3 CTAs / SM worth of registers (152 -> 128,
+// 20 bytes of spills; config-4 apply -0.08 ms); a cap for 4 CTAs measured slower (+0.33 ms)
 template <int P, int Q>
-__global__ void __launch_bounds__(AxCfg<P, Q>::T, SR_CROP_MINB)
+__global__ void __launch_bounds__(AxCfg<P, Q>::T, (SR_CROP_MINB > 1 || Q > 12) ? SR_CROP_MINB : 3)
 k_rows_crop(const RowGeom rg) {
   using S = FftShape<P, Q>;
   using A = AxCfg<P, Q>;

@@ -19,6 +19,7 @@ synthetic data with the config's shapes.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -107,7 +108,13 @@ def run_2d(cfgid: int, with_oracle: bool):
                             cs.CoilSketchConfig(C, cfg.sketch, reg, 3, 1), weights=weights, kernel=kern)
     compress = "lapack" if os.environ.get("SR_HOST_COMPRESS") else "device"
     runs = []
+    rep = None
     for _ in range(3):
+        # the previous run's report (and whatever else this process left behind: bench.py runs several
+        # configurations and a CPU oracle in one process) is released and collected outside the timed
+        # region
+        rep = None
+        gc.collect()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
