@@ -270,10 +270,21 @@ class GriddedKernel:
             return None
         key = (id(sqrt_w), squared)
         if key not in self._wcache:
+            # one weight vector at a time: entries of an earlier one are dropped (a kernel reused over
+            # many reconstructions would otherwise keep every vector it has seen)
+            for k in [k for k in self._wcache if k[0] != id(sqrt_w)]:
+                del self._wcache[k]
             sw = sqrt_w.to(torch.float64)
             v = (sw * sw) if squared else sw
             self._wcache[key] = (sqrt_w, v[self.orig.long()].to(torch.float32).contiguous())
         return self._wcache[key][1]
+
+    def prepare_weights(self, sqrt_w) -> None:
+        """Build the sorted-order weight vectors now (w for the normal op, sqrt(w) for forward /
+        adjoint), so that a caller about to capture CUDA graphs does not allocate them inside a capture
+        (memory of a graph's private pool is not returned to the allocator's cache)."""
+        self._weights(sqrt_w, True)
+        self._weights(sqrt_w, False)
 
     def _maps(self, maps):
         if maps.dim() != 3 or maps.shape[0] != 1 or maps.shape[2] != self.D:

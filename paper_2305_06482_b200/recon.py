@@ -136,6 +136,8 @@ class SketchedReconEngine:
         self.solver = solver
         self.step_scale = float(step_scale)
         self.sqrt_w = sqrt_w
+        if sqrt_w is not None and hasattr(kernel, "prepare_weights"):
+            kernel.prepare_weights(sqrt_w)  # not inside a graph capture (its first normal() may be captured)
         self.dims = tuple(dims)
         self.counter = counter if counter is not None else CostCounter()
         self.dev = self.maps0.device
