@@ -323,9 +323,12 @@ k_rowinv(float2* __restrict__ ws, const float2* __restrict__ maps,
 
 // ------------------------------------------------------------------- pass B
 
+#ifndef SR_COL_CB16
+#define SR_COL_CB16 16  // columns per CTA of the column pass for P >= 16
+#endif
 template <int P, int Q>
 struct ColCfg {
-  static constexpr int CB = (P >= 16) ? 16 : (P >= 4 ? 32 : 64);
+  static constexpr int CB = (P >= 16) ? SR_COL_CB16 : (P >= 4 ? 32 : 64);
   static constexpr int T = CB * P;
   static constexpr int VSP = FftShape<P, Q>::VS0 | 1;  // odd stride: conflict-free over columns
 };
