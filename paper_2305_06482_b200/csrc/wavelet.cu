@@ -29,6 +29,16 @@ __constant__ float c_hi[8] = {
     0.027983769416859854211f, -0.18703481171909308408f, -0.030841381835560763627f,
     0.032883011666885199735f, 0.010597401785069032105f};
 
+// the same taps as compile-time constants (immediate operands where the tap index is known)
+__device__ __forceinline__ constexpr float k_lo(int k) {
+  return k == 0 ? -0.010597401785069032105f : k == 1 ? 0.032883011666885199735f
+       : k == 2 ? 0.030841381835560763627f : k == 3 ? -0.18703481171909308408f
+       : k == 4 ? -0.027983769416859854211f : k == 5 ? 0.63088076792985890788f
+       : k == 6 ? 0.71484657055291564709f : 0.23037781330889650086f;
+}
+// hi[k] = (-1)^k lo[7 - k]
+__device__ __forceinline__ constexpr float k_hi(int k) { return (k & 1) ? -k_lo(7 - k) : k_lo(7 - k); }
+
 __device__ __forceinline__ float2 soft(float2 v, float t) {
   // v * max(|v| - t, 0) / |v|, zeros stay zero
   const float m = sqrtf(v.x * v.x + v.y * v.y);
@@ -155,6 +165,18 @@ k_wav_syn2(const float2* __restrict__ coef, float2* __restrict__ out, int h, int
   const float2* cb = coef + b * bs;
   const int tid = threadIdx.x;
   const bool interior = ci0 >= 0 && ci0 + SR_ <= hh && cj0 >= 0 && cj0 + SC_ <= hw;
+  if (interior && cj0 >= 1 && !(ld & 1) && !(hw & 1) && !(reinterpret_cast<size_t>(cb) & 15)) {
+    // interior tile, even row stride and quadrant offset: rows of 20 cells from the even column
+    // cj0 - 1 as ten 16-byte loads (the first cell is outside the tile)
+    for (int e = tid; e < 4 * SR_ * 10; e += 256) {
+      const int row = e / 10, pr = e - row * 10;
+      const int qd = row / SR_, r = row - qd * SR_;
+      const int oi = (qd & 2) ? hh : 0, oj = (qd & 1) ? hw : 0;
+      const float4 v = *reinterpret_cast<const float4*>(cb + (long long)(oi + ci0 + r) * ld + oj + cj0 - 1 + 2 * pr);
+      if (pr > 0) q[qd][r][2 * pr - 1] = make_float2(v.x, v.y);
+      q[qd][r][2 * pr] = make_float2(v.z, v.w);
+    }
+  } else
   for (int e = tid; e < 4 * SR_ * SC_; e += 256) {
     const int qd = e / (SR_ * SC_);
     const int rem = e - qd * SR_ * SC_;
@@ -164,46 +186,60 @@ k_wav_syn2(const float2* __restrict__ coef, float2* __restrict__ out, int h, int
     q[qd][r][c] = cb[(long long)(oi + gi) * ld + oj + gj];
   }
   __syncthreads();
+  // Each task makes the two outputs of a pair (even, odd position): they read the same four
+  // coefficients per band (position j + 3 - t of the tile for taps k = 2t and 2t + 1), so the loads are
+  // shared and every filter tap is a compile-time constant (the per-output form indexed the
+  // coefficient tables by the output's parity).  Accumulation order per output as before.
   // undo axis 1: u_lo0[r][n] from (LL, LH); u_hi0[r][n] from (HL, HH)
-  for (int e = tid; e < SR_ * SN; e += 256) {
-    const int r = e / SN, nn = e - r * SN;
-    const int n = n0 + nn;
-    const int par = n & 1;
-    float2 a = make_float2(0.f, 0.f), c = a;
+  for (int e = tid; e < SR_ * (SN / 2); e += 256) {
+    const int r = e / (SN / 2), jp = e - r * (SN / 2);
+    float2 ae = make_float2(0.f, 0.f), ce = ae, ao = ae, co = ae;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const int k = par + 2 * t;
-      const int jj = (n - k) / 2 - cj0;  // (n-k) even and >= n0-7 > 2*cj0 - 1
-      const float fl = c_lo[k], fh = c_hi[k];
+      const int jj = jp + 3 - t;  // ((n0 + 2 jp [+ 1]) - k) / 2 - cj0
       const float2 ll = q[0][r][jj], lh = q[1][r][jj], hl = q[2][r][jj], h2 = q[3][r][jj];
-      a.x = fmaf(fl, ll.x, fmaf(fh, lh.x, a.x)); a.y = fmaf(fl, ll.y, fmaf(fh, lh.y, a.y));
-      c.x = fmaf(fl, hl.x, fmaf(fh, h2.x, c.x)); c.y = fmaf(fl, hl.y, fmaf(fh, h2.y, c.y));
+      ae.x = fmaf(k_lo(2 * t), ll.x, fmaf(k_hi(2 * t), lh.x, ae.x));
+      ae.y = fmaf(k_lo(2 * t), ll.y, fmaf(k_hi(2 * t), lh.y, ae.y));
+      ce.x = fmaf(k_lo(2 * t), hl.x, fmaf(k_hi(2 * t), h2.x, ce.x));
+      ce.y = fmaf(k_lo(2 * t), hl.y, fmaf(k_hi(2 * t), h2.y, ce.y));
+      ao.x = fmaf(k_lo(2 * t + 1), ll.x, fmaf(k_hi(2 * t + 1), lh.x, ao.x));
+      ao.y = fmaf(k_lo(2 * t + 1), ll.y, fmaf(k_hi(2 * t + 1), lh.y, ao.y));
+      co.x = fmaf(k_lo(2 * t + 1), hl.x, fmaf(k_hi(2 * t + 1), h2.x, co.x));
+      co.y = fmaf(k_lo(2 * t + 1), hl.y, fmaf(k_hi(2 * t + 1), h2.y, co.y));
     }
-    ulo[r][nn] = a;
-    uhi[r][nn] = c;
+    ulo[r][2 * jp] = ae;
+    ulo[r][2 * jp + 1] = ao;
+    uhi[r][2 * jp] = ce;
+    uhi[r][2 * jp + 1] = co;
   }
   __syncthreads();
   float2* ob = out + b * bs;
-  for (int e = tid; e < SM * SN; e += 256) {
-    const int mm = e / SN, nn = e - mm * SN;
-    const int m = m0 + mm, n = n0 + nn;
-    if (m >= h || n >= w) continue;
-    const int par = m & 1;
-    float2 v = make_float2(0.f, 0.f);
+  for (int e = tid; e < (SM / 2) * SN; e += 256) {
+    const int ip = e / SN, nn = e - ip * SN;
+    const int m = m0 + 2 * ip, n = n0 + nn;
+    if (m >= h || n >= w) continue;  // h even: row m + 1 is inside with row m
+    const long long off = (long long)m * ld + n;
+    float2 xe = make_float2(0.f, 0.f), xo = xe;
+    if (zout) {  // issued before the taps: the loads are in flight while they run
+      xe = xold[b * bs + off];
+      xo = xold[b * bs + off + ld];
+    }
+    float2 ve = make_float2(0.f, 0.f), vo = ve;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const int k = par + 2 * t;
-      const int ii = (m - k) / 2 - ci0;
+      const int ii = ip + 3 - t;
       const float2 a = ulo[ii][nn], c = uhi[ii][nn];
-      v.x = fmaf(c_lo[k], a.x, fmaf(c_hi[k], c.x, v.x));
-      v.y = fmaf(c_lo[k], a.y, fmaf(c_hi[k], c.y, v.y));
+      ve.x = fmaf(k_lo(2 * t), a.x, fmaf(k_hi(2 * t), c.x, ve.x));
+      ve.y = fmaf(k_lo(2 * t), a.y, fmaf(k_hi(2 * t), c.y, ve.y));
+      vo.x = fmaf(k_lo(2 * t + 1), a.x, fmaf(k_hi(2 * t + 1), c.x, vo.x));
+      vo.y = fmaf(k_lo(2 * t + 1), a.y, fmaf(k_hi(2 * t + 1), c.y, vo.y));
     }
-    const long long off = (long long)m * ld + n;
     if (zout) {
-      const float2 xo = xold[b * bs + off];
-      zout[b * bs + off] = make_float2(fmaf(beta, v.x - xo.x, v.x), fmaf(beta, v.y - xo.y, v.y));
+      zout[b * bs + off] = make_float2(fmaf(beta, ve.x - xe.x, ve.x), fmaf(beta, ve.y - xe.y, ve.y));
+      zout[b * bs + off + ld] = make_float2(fmaf(beta, vo.x - xo.x, vo.x), fmaf(beta, vo.y - xo.y, vo.y));
     }
-    ob[off] = v;
+    ob[off] = ve;
+    ob[off + ld] = vo;
   }
 }
 
