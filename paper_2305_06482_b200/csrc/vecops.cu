@@ -12,7 +12,15 @@
 namespace {
 
 constexpr int RED_THREADS = 256;
-constexpr int RED_BLOCKS = 64;  // partial sums per slice (fixed => deterministic)
+// Partial sums per slice: a function of the vector length only (>= 2048 elements per block, 16..592
+// blocks), so a reduction is deterministic and independent of the batch, and a single long vector
+// (config 4: 84 MB images, 2.4 GB sample arrays) is read by the whole GPU -- 64 blocks per slice read
+// such a vector at ~1 TB/s.  Callers size their partial buffers with sr_reduce_nparts() (the maximum).
+constexpr int RED_BLOCKS_MAX = 592;
+static inline int red_blocks(long long n) {
+  const long long nb = n / 2048;
+  return (int)(nb < 16 ? 16 : (nb > RED_BLOCKS_MAX ? RED_BLOCKS_MAX : nb));
+}
 
 enum { RED_NORM2 = 0, RED_DOT = 1, RED_ABS = 2, RED_DIFF2 = 3 };
 
@@ -235,9 +243,9 @@ k_cg_p(float2* __restrict__ p, const float2* __restrict__ r, const double2* __re
 
 extern "C" {
 
-int sr_reduce_nparts(void) { return RED_BLOCKS; }
+int sr_reduce_nparts(void) { return RED_BLOCKS_MAX; }
 
-// Fused CG vector step (see k_cg_xr / k_cg_p): after mp = M p.  pdot, prs: (batch, RED_BLOCKS)
+// Fused CG vector step (see k_cg_xr / k_cg_p): after mp = M p.  pdot, prs: (batch, sr_reduce_nparts())
 // double2 scratch; state: (batch, 4) double [rs0, rs1, active, iterations] initialised by the
 // caller (rs0 = |r0|^2, active = 1, iterations = 0); parity = iteration index & 1; hist: NULL or
 // (batch, hist_len + 1) doubles receiving sqrt(rs) after iteration it at [it].
@@ -246,7 +254,8 @@ int sr_cg_step(sr_c64* x, sr_c64* r, sr_c64* p, const sr_c64* mp, double* pdot, 
                double tol_abs, void* stream) {
   if (n < 0 || batch < 1 || !x || !r || !p || !mp || !pdot || !prs || !state || (parity & ~1)) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid(RED_BLOCKS, batch);
+  const int nblk = red_blocks(n);
+  dim3 grid(nblk, batch);
   k_reduce_partial<<<grid, RED_THREADS, 0, st>>>(RED_DOT, (const float2*)p, (const float2*)mp, n, bstride,
                                                  (double2*)pdot);
   SR_CHECK_LAUNCH();
@@ -259,17 +268,18 @@ int sr_cg_step(sr_c64* x, sr_c64* r, sr_c64* p, const sr_c64* mp, double* pdot, 
   return SR_OK;
 }
 
-// partial: (batch, RED_BLOCKS) double2 workspace; result: (batch,) double2
+// partial: (batch, sr_reduce_nparts()) double2 workspace; result: (batch,) double2
 int sr_reduce(int mode, const sr_c64* a, const sr_c64* b, long long n, long long bstride,
               int batch, double* partial, double* result, void* stream) {
   if (n < 0 || batch < 1 || mode < 0 || mode > 3) return SR_EINVAL;
   if ((mode == RED_DOT || mode == RED_DIFF2) && b == nullptr) return SR_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  dim3 grid(RED_BLOCKS, batch);
+  const int nblk = red_blocks(n);
+  dim3 grid(nblk, batch);
   k_reduce_partial<<<grid, RED_THREADS, 0, st>>>(mode, (const float2*)a, (const float2*)b, n,
                                                  bstride, (double2*)partial);
   SR_CHECK_LAUNCH();
-  k_reduce_final<<<(batch + 127) / 128, 128, 0, st>>>((const double2*)partial, RED_BLOCKS, batch,
+  k_reduce_final<<<(batch + 127) / 128, 128, 0, st>>>((const double2*)partial, nblk, batch,
                                                       (double2*)result);
   SR_CHECK_LAUNCH();
   return SR_OK;
