@@ -18,15 +18,6 @@
 
 namespace {
 
-__constant__ float c_lo[8] = {
-    -0.010597401785069032105f, 0.032883011666885199735f, 0.030841381835560763627f,
-    -0.18703481171909308408f, -0.027983769416859854211f, 0.63088076792985890788f,
-    0.71484657055291564709f, 0.23037781330889650086f};
-__constant__ float c_hi[8] = {
-    0.23037781330889650086f, -0.71484657055291564709f, 0.63088076792985890788f,
-    0.027983769416859854211f, -0.18703481171909308408f, -0.030841381835560763627f,
-    0.032883011666885199735f, 0.010597401785069032105f};
-
 struct AxisArgs {
   const float2* src;
   float2* dst;
@@ -56,67 +47,101 @@ __device__ __forceinline__ int pwrap(int j, int p) {
   return j;
 }
 
+// filter taps as compile-time constants (hi[k] = (-1)^k lo[7 - k])
+__device__ __forceinline__ constexpr float k_lo(int k) {
+  return k == 0 ? -0.010597401785069032105f : k == 1 ? 0.032883011666885199735f
+       : k == 2 ? 0.030841381835560763627f : k == 3 ? -0.18703481171909308408f
+       : k == 4 ? -0.027983769416859854211f : k == 5 ? 0.63088076792985890788f
+       : k == 6 ? 0.71484657055291564709f : 0.23037781330889650086f;
+}
+__device__ __forceinline__ constexpr float k_hi(int k) { return (k & 1) ? -k_lo(7 - k) : k_lo(7 - k); }
+
+// One work item makes an output PAIR along the axis from shared loads: analysis item i reads the 8
+// inputs 2i .. 2i + 7 once for the low-pass output i and the high-pass output hn + i; synthesis item j
+// reads lo / hi at j, j - 1, j - 2, j - 3 once for the outputs 2j and 2j + 1 (taps 2t and 2t + 1).  The
+// per-output form loaded 8 values per output and indexed the tap tables by the output's band / parity.
 __global__ void __launch_bounds__(256) k_wav_axis(AxisArgs a) {
   const int b = blockIdx.y;
-  // a level corner holds < 2^31 elements (the kernel indexes it in 32-bit; see sr_wavelet_axis)
-  const int total = a.h[0] * a.h[1] * a.h[2];
   const int ax = a.axis;
   const int n = a.h[ax], hn = n >> 1;
+  // items: the level corner with the extent along `ax` halved (< 2^30, see sr_wavelet_axis)
+  int hx[3] = {a.h[0], a.h[1], a.h[2]};
+  hx[ax] = hn;
+  const int total = hx[0] * hx[1] * hx[2];
   const long long sa = a.st[ax];
   const float2* src = a.src + b * a.bs;
   float2* dst = a.dst + b * a.bs;
   double part = 0.0;
   const float t = a.thresh ? a.thresh[b] : a.hthresh;
+  const bool thr = a.thresh || a.hthresh >= 0.f;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int q = e / a.h[2];
-    const int i2 = e - q * a.h[2];
-    const int i0 = q / a.h[1];
-    const int i1 = q - i0 * a.h[1];
+    const int q = e / hx[2];
+    const int i2 = e - q * hx[2];
+    const int i0 = q / hx[1];
+    const int i1 = q - i0 * hx[1];
     const int ii[3] = {i0, i1, i2};
-    const long long off = i0 * a.st[0] + i1 * a.st[1] + i2 * a.st[2];
-    const long long line = off - (long long)ii[ax] * sa;  // start of this line along `ax`
-    const int m = ii[ax];
-    float2 v = make_float2(0.f, 0.f);
+    const int i = ii[ax];
+    const long long line = i0 * a.st[0] + i1 * a.st[1] + i2 * a.st[2] - (long long)i * sa;  // start of the line along `ax`
     if (!a.inverse) {
-      const bool is_hi = m >= hn;
-      const int i = is_hi ? m - hn : m;
+      float2 lo = make_float2(0.f, 0.f), hi = lo;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float f = is_hi ? c_hi[k] : c_lo[k];
         const float2 x = src[line + (long long)pwrap(2 * i + k, n) * sa];
-        v.x = fmaf(f, x.x, v.x);
-        v.y = fmaf(f, x.y, v.y);
+        lo.x = fmaf(k_lo(k), x.x, lo.x);
+        lo.y = fmaf(k_lo(k), x.y, lo.y);
+        hi.x = fmaf(k_hi(k), x.x, hi.x);
+        hi.y = fmaf(k_hi(k), x.y, hi.y);
       }
       if (a.thr_enable) {
+        // the high-pass output is a detail coefficient; the low-pass one is final only outside the
+        // low-pass corner of the other axes, or at the last level
         bool lowpass = true;
 #pragma unroll
         for (int d = 0; d < 3; ++d)
-          if (a.h[d] > 1 && ii[d] >= (a.h[d] >> 1)) lowpass = false;
-        const bool final_coef = !lowpass || a.last_level;
-        if (final_coef && (a.thresh || a.hthresh >= 0.f)) {
-          const float mg = sqrtf(v.x * v.x + v.y * v.y);
-          const float s = (mg > t) ? (mg - t) / mg : 0.f;
-          v = make_float2(v.x * s, v.y * s);
+          if (d != ax && a.h[d] > 1 && ii[d] >= (a.h[d] >> 1)) lowpass = false;
+        const bool lo_final = !lowpass || a.last_level;
+        if (thr) {
+          const float mh = sqrtf(hi.x * hi.x + hi.y * hi.y);
+          const float sh = (mh > t) ? (mh - t) / mh : 0.f;
+          hi = make_float2(hi.x * sh, hi.y * sh);
+          if (lo_final) {
+            const float ml = sqrtf(lo.x * lo.x + lo.y * lo.y);
+            const float sl = (ml > t) ? (ml - t) / ml : 0.f;
+            lo = make_float2(lo.x * sl, lo.y * sl);
+          }
         }
-        if (final_coef && a.l1part) part += sqrt((double)v.x * v.x + (double)v.y * v.y);
+        if (a.l1part) {
+          if (lo_final) part += sqrt((double)lo.x * lo.x + (double)lo.y * lo.y);
+          part += sqrt((double)hi.x * hi.x + (double)hi.y * hi.y);
+        }
       }
+      dst[line + (long long)i * sa] = lo;
+      dst[line + (long long)(hn + i) * sa] = hi;
     } else {
-      const int par = m & 1;
+      const long long oe = line + (long long)(2 * i) * sa, oo = oe + sa;
+      float2 xe = make_float2(0.f, 0.f), xo = xe;
+      if (a.zout) {
+        xe = a.xold[b * a.bs + oe];
+        xo = a.xold[b * a.bs + oo];
+      }
+      float2 ve = make_float2(0.f, 0.f), vo = ve;
 #pragma unroll
       for (int tt = 0; tt < 4; ++tt) {
-        const int k = par + 2 * tt;
-        const int i = pwrap((m - k) / 2, hn);
-        const float2 lo = src[line + (long long)i * sa];
-        const float2 hi = src[line + (long long)(hn + i) * sa];
-        v.x = fmaf(c_lo[k], lo.x, fmaf(c_hi[k], hi.x, v.x));
-        v.y = fmaf(c_lo[k], lo.y, fmaf(c_hi[k], hi.y, v.y));
+        const int p = pwrap(i - tt, hn);
+        const float2 lo = src[line + (long long)p * sa];
+        const float2 hi = src[line + (long long)(hn + p) * sa];
+        ve.x = fmaf(k_lo(2 * tt), lo.x, fmaf(k_hi(2 * tt), hi.x, ve.x));
+        ve.y = fmaf(k_lo(2 * tt), lo.y, fmaf(k_hi(2 * tt), hi.y, ve.y));
+        vo.x = fmaf(k_lo(2 * tt + 1), lo.x, fmaf(k_hi(2 * tt + 1), hi.x, vo.x));
+        vo.y = fmaf(k_lo(2 * tt + 1), lo.y, fmaf(k_hi(2 * tt + 1), hi.y, vo.y));
       }
       if (a.zout) {
-        const float2 xo = a.xold[b * a.bs + off];
-        a.zout[b * a.bs + off] = make_float2(fmaf(a.beta, v.x - xo.x, v.x), fmaf(a.beta, v.y - xo.y, v.y));
+        a.zout[b * a.bs + oe] = make_float2(fmaf(a.beta, ve.x - xe.x, ve.x), fmaf(a.beta, ve.y - xe.y, ve.y));
+        a.zout[b * a.bs + oo] = make_float2(fmaf(a.beta, vo.x - xo.x, vo.x), fmaf(a.beta, vo.y - xo.y, vo.y));
       }
+      dst[oe] = ve;
+      dst[oo] = vo;
     }
-    dst[off] = v;
   }
   if (a.l1part) {
     __shared__ double red[256];
@@ -164,7 +189,7 @@ int sr_wavelet_axis(const sr_c64* src, sr_c64* dst, int h0, int h1, int h2, int 
   a.beta = beta;
   // without per-block partials the grid is 2368 blocks (measured on the config-4 prox: 592
   // blocks 1.17 ms, 1184 1.20, 2368 1.04, 4736 1.08, one element per thread 1.49 ms)
-  const long long total = (long long)h0 * h1 * h2;
+  const long long total = (long long)h0 * h1 * h2 / 2;  // one work item per output pair along the axis
   long long nb = l1part ? sr_wavelet_axis_nblocks() : min((total + 255) / 256, (long long)SR_WAV_AXIS_GRID);
   if (nb > 0x7fffffffLL) nb = 0x7fffffffLL;
   dim3 grid((unsigned)nb, batch);
