@@ -187,8 +187,9 @@ int sr_wavelet_axis(const sr_c64* src, sr_c64* dst, int h0, int h1, int h2, int 
   a.zout = (float2*)zout;
   a.xold = (const float2*)xold;
   a.beta = beta;
-  // without per-block partials the grid is 2368 blocks (measured on the config-4 prox: 592
-  // blocks 1.17 ms, 1184 1.20, 2368 1.04, 4736 1.08, one element per thread 1.49 ms)
+  // without per-block partials the grid is 2368 blocks (config-4 prox with the pair kernel: 1184
+  // blocks 0.663 ms, 2368 0.672, 4736 0.659 -- flat; the per-output kernel had measured 592 blocks
+  // 1.17 ms, 2368 1.04, one element per thread 1.49 ms)
   const long long total = (long long)h0 * h1 * h2 / 2;  // one work item per output pair along the axis
   long long nb = l1part ? sr_wavelet_axis_nblocks() : min((total + 255) / 256, (long long)SR_WAV_AXIS_GRID);
   if (nb > 0x7fffffffLL) nb = 0x7fffffffLL;
