@@ -308,9 +308,9 @@ class GriddedKernel:
             # large grids: two spread grids used in turn, the idle one zeroed while the gridding kernel
             # runs (the state is the pair (coil count, clean spread grid); any other workspace user
             # resets it)
-            pp = self._pp
+            pp, before = self._pp, self._grids
             grids = self.workspace(C, normal=True, slots=3)
-            idx, clean = (pp[1], 1) if pp is not None and pp[0] == C else (0, 0)
+            idx, clean = (pp[1], 1) if pp is not None and pp[0] == C and grids is before else (0, 0)
             _lib.call("sr_nufft_normal_pp", dv.ptr(x), dv.ptr(anchor), dv.ptr(maps), C, *self._geom()[:4],
                       *self._geom()[4:], dv.ptr(self.base), dv.ptr(self.frac), dv.ptr(self._weights(w, True)),
                       self.n_points, dv.ptr(out), dv.ptr(grids), dv.ptr(coef), dv.ptr(u), dv.ptr(d), *self._bins(),
