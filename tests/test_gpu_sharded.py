@@ -143,6 +143,24 @@ def test_nufft_normal_slabs_equal_normal(cuda):
         small.normal_slabs(m2, x2, torch.empty_like(x2), [(0, 10), (10, 20)], lambda lo, hi: None)
 
 
+def test_nufft_coil_looped_embed_equals_one_shot(cuda):
+    """The embed + row FFT pass with the coils looped inside the CTA (several coils, enough image rows)
+    == the one-shot pass (taken for a single coil): the normal op over C coils equals the sum of the
+    C single-coil normal ops, with and without the anchor."""
+    kern, maps, x, _ = _slab_problem(cuda)
+    a = torch.randn_like(x) * 0.1
+    for kw in ({}, dict(anchor=a)):
+        full = torch.empty_like(x)
+        kern.normal(maps, x, full, **kw)
+        acc = torch.zeros_like(x)
+        one = torch.empty_like(x)
+        for j in range(maps.shape[1]):
+            kern.normal(maps[:, j:j + 1].contiguous(), x, one, **kw)
+            acc += one
+        err = float(torch.linalg.vector_norm(full - acc) / torch.linalg.vector_norm(acc))
+        assert err < 2e-6, (list(kw), err)
+
+
 def test_nufft_normal_pingpong_equals_normal(cuda):
     """The normal op with two spread grids used in turn (the idle one zeroed on a library stream while
     the gridding kernel runs, sr_nufft_normal_pp) == the one-grid normal op, over a run of calls with
